@@ -1,0 +1,334 @@
+"""The barrier-augmented Lagrangian time step (Alg. 1) with its inexact
+Newton-PCG primal solve (§4) -- the oracle procedure of SURVEY.md §8(c) c.1.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+Per time step (backward Euler):  y = x_t + h v_t + h^2 G;  x^0 = x_t (Q5);
+mu = {}, A' = {} (Alg. 1 data line); sigma^0 from the least-squares fit (Q7).
+Per Newton iteration l (one inexact Newton iteration = one l, Q6):
+  A = {d < dhat at x^l}; dmin; A' rules (Alg. 1 lines 3-6; Q9, Q10)
+  friction anchors at x^l (Q25, Q26)
+  e = grad L (line 7); assemble A, Lambda, groups; warm start; PCG (App. B) -> p
+  line search: alpha_0 = min(1, alpha_CCD), halve on energy increase / budget (Q35-Q37),
+    alpha < 1e-9 -> resume PCG +100 iterations (App. B, Q16)
+  x^{l+1} = x^l + alpha p;  stop if ||e^l|| <= 1e-4 ||e^0|| (lines 9-11; Q13)
+  s_i, mu_i on A' (lines 12-14; Q11, Q12);  sigma <- max(1.2 sigma, 100 sigma^0) if min d < 1e-2 dhat
+  (lines 15-16; Q8)
+v_{t+1} = (x_{t+1} - x_t)/h (eq:int:x).
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import ccd as ccdm
+from . import contact as cm
+from . import linalg as la
+from .assemble import floor_log10
+from .energy import barrier, inertia_energy, inertia_grad, nh_energy, nh_stencils
+from .mesh import precompute
+from .projection import project_eigh
+
+FLAG_NO_WARMSTART = 1
+FLAG_NO_AUGLAG = 2
+
+
+class NotConverged(RuntimeError):
+    pass
+
+
+def _coo_add(rows, cols, vals, ids, H):
+    k = len(ids)
+    dof = (3 * np.asarray(ids)[:, None] + np.arange(3)[None]).ravel()
+    rows.append(np.repeat(dof, 3 * k))
+    cols.append(np.tile(dof, 3 * k))
+    vals.append(H.ravel())
+
+
+class Oracle:
+    def __init__(self, scene, flags=0):
+        self.scene = scene
+        self.mesh = precompute(scene)
+        p = scene["params"]
+        self.p = p
+        self.h = float(p["h"])
+        self.g = np.asarray(p["gravity"], np.float64)
+        self.dhat = float(p["dhat"])
+        self.flags = flags
+        self.free = ~self.mesh.fixed
+        self.N = self.mesh.n
+
+    # ------------------------------------------------------------------ energy
+    def energy(self, x, st, pt, ee):
+        """L(x) at fixed (y, sigma, A' with mu, s, friction anchors); returns (L, n_constraints)."""
+        m = self.mesh
+        if m.tets.size and nh_energy(x, m) == np.inf:
+            return np.inf, 0
+        keys, d = cm.constraint_set(x, pt, ee, self.dhat)
+        if len(d) and np.min(d) <= 0.0:
+            return np.inf, len(d)
+        dap = cm.key_distance(x, st["ap_keys"]) if len(st["ap_keys"]) else np.zeros(0)
+        if len(dap) and np.min(dap) <= 0.0:
+            return np.inf, len(d)
+        L = inertia_energy(x, st["y"], m.mass, self.h, self.free) + nh_energy(x, m)
+        L += float(np.sum(st["sigma"] * barrier(d, self.dhat)))
+        if len(dap):
+            L += float(np.sum(cm.phi_energy(dap, np.zeros(len(dap)), np.ones(len(dap)),
+                                            st["ap_mu"], st["ap_s"], st["sigma"], self.dhat)))
+        if st.get("fr_keys") is not None and len(st["fr_keys"]):
+            L += cm.friction_energy(x, st["x_t"], st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"],
+                                    float(self.p["chi"]), float(self.p["eps_v"]), self.h)
+        if not np.isfinite(L):
+            return np.inf, len(d)
+        return L, len(d)
+
+    # ---------------------------------------------------------------- stencils
+    def contact_stencil_set(self, x, keys_A, st):
+        """Merge A (resolved at x) and A' keys into one stencil list (Q22)."""
+        ap = st["ap_keys"]
+        allk = np.concatenate([keys_A, ap]) if len(ap) else keys_A
+        if len(allk) == 0:
+            return np.zeros((0, 5), np.int64), np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0)
+        uk, inv = np.unique(allk, axis=0, return_inverse=True)
+        inv = inv.ravel()
+        inA = np.zeros(len(uk))
+        inA[inv[:len(keys_A)]] = 1.0
+        inAp = np.zeros(len(uk))
+        mu = np.zeros(len(uk))
+        s = np.zeros(len(uk))
+        if len(ap):
+            ia = inv[len(keys_A):]
+            inAp[ia] = 1.0
+            mu[ia] = st["ap_mu"]
+            s[ia] = st["ap_s"]
+        return uk, inA, inAp, mu, s
+
+    def assemble(self, x, st, keys_A):
+        """Returns dict with CSR A (fixed rows identity), gradient e, Dinv, e_j, groups, stencils."""
+        m = self.mesh
+        N, h = self.N, self.h
+        rows, cols, vals = [], [], []
+        grad = inertia_grad(x, st["y"], m.mass, h, np.ones(N, bool)).ravel()
+        lam_diag = np.repeat(m.mass / (h * h), 3).reshape(N, 3).copy()
+        # inertia
+        dm = np.repeat(m.mass / (h * h), 3)
+        rows.append(np.arange(3 * N))
+        cols.append(np.arange(3 * N))
+        vals.append(dm)
+        out = {}
+        # elastic (AD Hessian, projected on the full 12x12; Q21, Q23)
+        if m.tets.size:
+            _v, g, H = nh_stencils(x, m)
+            P, wc = project_eigh(H)
+            lb = wc.sum(axis=1) / 12.0
+            for k in range(4):
+                np.add.at(grad.reshape(N, 3), m.tets[:, k], g[:, 3 * k:3 * k + 3])
+                np.add.at(lam_diag, m.tets[:, k], lb[:, None])
+            dof = (3 * m.tets[:, :, None] + np.arange(3)[None, None]).reshape(-1, 12)
+            rows.append(np.repeat(dof, 12, axis=1).ravel())
+            cols.append(np.tile(dof, (1, 12)).ravel())
+            vals.append(P.reshape(-1))
+            out["elastic_P"] = P
+            out["elastic_lbar"] = lb
+        # contact
+        uk, inA, inAp, mu, s = self.contact_stencil_set(x, keys_A, st)
+        cs = cm.contact_stencils(x, uk, inA, inAp, mu, s, st["sigma"], self.dhat) if len(uk) else []
+        c_P, c_lb = [], []
+        for (ids, g, H, _d, _dp) in cs:
+            P, wc = project_eigh(H[None])
+            lb = wc.sum() / (3 * len(ids))
+            grad.reshape(N, 3)[ids] += g.reshape(-1, 3)
+            lam_diag[ids] += lb
+            _coo_add(rows, cols, vals, ids, P[0])
+            c_P.append(P[0])
+            c_lb.append(lb)
+        out["contact_keys"], out["contact_P"], out["contact_lbar"] = uk, c_P, c_lb
+        out["contact_inA"], out["contact_inAp"] = inA, inAp
+        # friction (PSD analytically; not projected, not in Lambda: Q17)
+        if st.get("fr_keys") is not None and len(st["fr_keys"]):
+            fs = cm.friction_stencils(x, st["x_t"], st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"],
+                                      float(self.p["chi"]), float(self.p["eps_v"]), h)
+            for (ids, g, H) in fs:
+                grad.reshape(N, 3)[ids] += g.reshape(-1, 3)
+                _coo_add(rows, cols, vals, ids, H)
+            out["friction"] = fs
+        A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                          shape=(3 * N, 3 * N)).tocsr()
+        A.sum_duplicates()
+        fixed_dof = np.repeat(m.fixed, 3)
+        if np.any(fixed_dof):
+            keep = sp.diags((~fixed_dof).astype(np.float64))
+            A = (keep @ A @ keep + sp.diags(fixed_dof.astype(np.float64))).tocsr()
+            grad[fixed_dof] = 0.0
+        A.eliminate_zeros()
+        Dblk = np.zeros((N, 3, 3))
+        for c1 in range(3):
+            for c2 in range(3):
+                Dblk[:, c1, c2] = np.asarray(A[3 * np.arange(N) + c1, 3 * np.arange(N) + c2]).ravel()
+        e_j = lam_diag.sum(axis=1)
+        groups = np.full(N, -999, np.int64)
+        groups[self.free] = floor_log10(e_j[self.free])
+        out.update(A=A, grad=grad, Dblk=Dblk, Dinv=np.linalg.inv(Dblk), e_j=e_j, groups=groups)
+        return out
+
+    # ------------------------------------------------------------- friction anchors
+    def friction_anchors(self, x, st, keys_A):
+        """lambda_j = -phi_j'(d_j) at x^l, Gamma, n (Q25, Q26); friction pairs = A at x^l."""
+        if float(self.p["chi"]) <= 0.0 or len(keys_A) == 0:
+            return None
+        uk, inA, inAp, mu, s = self.contact_stencil_set(x, keys_A, st)
+        sel = inA > 0
+        keys = uk[sel]
+        d = cm.key_distance(x, keys)
+        dphi = cm._dphi(d, inA[sel], inAp[sel], mu[sel], s[sel], st["sigma"], self.dhat)
+        G, n = cm.closest_point_weights(x, keys)
+        return keys, G, n, -dphi
+
+    # -------------------------------------------------------------------- sigma0
+    def sigma0(self, x, st, keys):
+        m = self.mesh
+        N = self.N
+        gE = inertia_grad(x, st["y"], m.mass, self.h, np.ones(N, bool)).ravel()
+        if m.tets.size:
+            _v, g, _H = nh_stencils(x, m)
+            for k in range(4):
+                np.add.at(gE.reshape(N, 3), m.tets[:, k], g[:, 3 * k:3 * k + 3])
+        gb = np.zeros(3 * N)
+        if len(keys):
+            cs = cm.contact_stencils(x, keys, np.ones(len(keys)), np.zeros(len(keys)), np.zeros(len(keys)),
+                                     np.zeros(len(keys)), 1.0, self.dhat)
+            for (ids, g, _H, _d, _dp) in cs:
+                gb.reshape(N, 3)[ids] += g.reshape(-1, 3)
+        fd = np.repeat(m.fixed, 3)
+        gE[fd] = 0.0
+        gb[fd] = 0.0
+        floor = float(np.mean(m.mass[self.free])) / (self.h * self.h)
+        bb = float(gb @ gb)
+        if bb == 0.0:
+            return floor
+        return max(-float(gb @ gE) / bb, floor)
+
+    # ---------------------------------------------------------------------- step
+    def step(self, x_t, v_t, trace=None):
+        p = self.p
+        m = self.mesh
+        h, dhat = self.h, self.dhat
+        x_t = np.asarray(x_t, np.float64).reshape(-1, 3)
+        v_t = np.asarray(v_t, np.float64).reshape(-1, 3)
+        y = x_t + h * v_t + h * h * self.g[None]
+        y[m.fixed] = x_t[m.fixed]
+        x = x_t.copy()
+        st = dict(y=y, x_t=x_t, ap_keys=np.zeros((0, 5), np.int64), ap_mu=np.zeros(0), ap_s=np.zeros(0),
+                  fr_keys=None)
+        pt, ee = cm.candidates(m, x, x, dhat)
+        keys, d = cm.constraint_set(x, pt, ee, dhat)
+        if len(d) and d.min() <= 0:
+            raise ValueError("infeasible input: surface distance <= 0")
+        sig0 = self.sigma0(x, st, keys)
+        st["sigma"] = sig0
+        dmin_prev = np.inf
+        e0 = None
+        stats = dict(newton=0, pcg=0, ws=0, max_constraints=0)
+        converged = False
+        for l in range(int(p["max_newton"])):
+            pt, ee = cm.candidates(m, x, x, dhat)
+            keys, d = cm.constraint_set(x, pt, ee, dhat)
+            dmin = float(d.min()) if len(d) else np.inf
+            rebuilt = False
+            if self.flags & FLAG_NO_AUGLAG:
+                pass
+            elif dmin > 1e-2 * dhat:
+                st["ap_keys"], st["ap_mu"], st["ap_s"] = np.zeros((0, 5), np.int64), np.zeros(0), np.zeros(0)
+            elif dmin < dmin_prev or len(st["ap_keys"]) == 0:
+                newk = keys[d < 1e-2 * dhat]
+                mu_new, s_new = np.zeros(len(newk)), np.zeros(len(newk))
+                old = {tuple(k): (mu_, s_) for k, mu_, s_ in zip(st["ap_keys"], st["ap_mu"], st["ap_s"])}
+                for i, k in enumerate(newk):
+                    if tuple(k) in old:
+                        mu_new[i], s_new[i] = old[tuple(k)]
+                st["ap_keys"], st["ap_mu"], st["ap_s"] = newk, mu_new, s_new
+                rebuilt = True
+            dmin_prev = dmin
+            fr = self.friction_anchors(x, st, keys)
+            if fr is not None:
+                st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"] = fr
+            else:
+                st["fr_keys"] = None
+            asm = self.assemble(x, st, keys)
+            e = asm["grad"]
+            en = float(np.linalg.norm(e))
+            if e0 is None:
+                e0 = en
+            if e0 == 0.0:
+                converged = True
+                break
+            A, Dinv = asm["A"], asm["Dinv"]
+            b = -e
+            ws_it = {}
+            if self.flags & FLAG_NO_WARMSTART:
+                x0 = np.zeros_like(b)
+            else:
+                x0, ws_it = la.warm_start(A, b, asm["groups"], Dinv, m.fixed, float(p["ws_rel_tol"]),
+                                          int(p["ws_max_iters"]))
+            pst = la.pcg(A, b, x0, Dinv, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
+                         int(p["max_pcg"]))
+            resumes = 0
+            while True:
+                dirn = pst.x.copy()
+                safeguard = False
+                if float(dirn @ e) >= 0.0:
+                    dirn = -la.apply_block(Dinv, e)
+                    safeguard = True
+                P = dirn.reshape(-1, 3)
+                cpt, cee = cm.candidates(m, x, x + P, dhat)
+                a_ccd = ccdm.step_toi(x, P, cpt, cee, dhat)
+                alpha = min(1.0, a_ccd)
+                L0, _n0 = self.energy(x, st, cpt, cee)
+                halvings = 0
+                while alpha >= float(p["alpha_min"]):
+                    L1, n1 = self.energy(x + alpha * P, st, cpt, cee)
+                    if n1 <= int(p["max_constraints"]) and L1 <= L0:
+                        break
+                    alpha *= 0.5
+                    halvings += 1
+                if alpha >= float(p["alpha_min"]):
+                    break
+                if resumes >= 50 or pst.k >= int(p["max_pcg"]):
+                    raise NotConverged("line search failed after PCG resumes")
+                resumes += 1
+                pst = la.pcg_run(A, Dinv, pst, 0.0, 10 ** 9, min(pst.k + int(p["pcg_resume_iters"]),
+                                                                  int(p["max_pcg"])))
+            x_new = x + alpha * P
+            stats["newton"] += 1
+            stats["pcg"] += pst.k
+            stats["ws"] += sum(ws_it.values()) if ws_it else 0
+            stats["max_constraints"] = max(stats["max_constraints"], len(keys))
+            if trace is not None:
+                gvals, gcnt = np.unique(asm["groups"][self.free], return_counts=True)
+                trace.append(dict(l=l, nA=len(keys), nAp=len(st["ap_keys"]), rebuilt=rebuilt, dmin=dmin,
+                                  sigma=st["sigma"], groups=dict(zip(gvals.tolist(), gcnt.tolist())),
+                                  ws_iters=ws_it, pcg_iters=pst.k, pcg_stop=pst.stop, alpha_ccd=a_ccd,
+                                  alpha=alpha, halvings=halvings, resumes=resumes, safeguard=safeguard,
+                                  rel_e=en / e0))
+            if en <= float(p["newton_rel_tol"]) * e0:
+                x = x_new
+                converged = True
+                break
+            # AL updates on A' (lines 12-14)
+            if len(st["ap_keys"]):
+                dn = cm.key_distance(x_new, st["ap_keys"])
+                s_new = np.maximum(-st["ap_mu"] / st["sigma"] - dhat + dn, 0.0)
+                st["ap_s"] = s_new
+                st["ap_mu"] = st["ap_mu"] + st["sigma"] * barrier(dn, dhat + s_new)
+            # sigma schedule (lines 15-16)
+            if not (self.flags & FLAG_NO_AUGLAG):
+                _k2, d2 = cm.constraint_set(x_new, cpt, cee, dhat)
+                if len(d2) and float(d2.min()) < 1e-2 * dhat:
+                    st["sigma"] = max(1.2 * st["sigma"], 100.0 * sig0)
+            x = x_new
+        if not converged:
+            raise NotConverged("Newton iteration cap reached")
+        x[m.fixed] = x_t[m.fixed]
+        v = (x - x_t) / h
+        stats["sigma0"] = sig0
+        return x, v, stats

@@ -1,0 +1,125 @@
+"""Linear algebra of the inexact Newton step: SpMV, block-Jacobi PCG with the App. B policy,
+and the stiffness-grouped block-Jacobi warm start.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+ - SpMV: y = (D + L + L^T + sum_i (C_i + C_i^T)) v, i.e. the plain product with the assembled
+   symmetric matrix (§5.1).  Here: scipy CSR product (library primitive).
+ - PCG: textbook preconditioned CG (Saad, Alg. 9.1) with M = blockdiag(D_j) (PAPER.md:384, 418
+   "block diagonal ... also used for preconditioning").  Stop (App. B):
+     ||r_k|| <= tol ||r^0||, r^0 := b (residual of the zero guess);
+     stagnation: k >= W and min_{k-W < j <= k} ||r_j|| >= min_{j <= k-W} ||r_j|| (Q15);
+     iteration cap; NaN.
+ - warm start: for each stiffness group G an
+   independent block-Jacobi PCG on A_GG (cross-group blocks skipped), zero initial guess,
+   stop at ||r_G|| <= ws_tol ||b_G|| or ws_max iterations; the union is the initial guess x_0.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+STOP_CONVERGED, STOP_STAGNATED, STOP_CAP, STOP_NAN = 0, 1, 2, 3
+
+
+def block_inverse(Dblocks):
+    return np.linalg.inv(Dblocks)
+
+
+def apply_block(Dinv, r):
+    N = Dinv.shape[0]
+    return np.einsum("nij,nj->ni", Dinv, r.reshape(N, 3)).ravel()
+
+
+class PCGState:
+    """Saved PCG state so App. B's 'return to PCG for an additional 100 iterations' can resume."""
+
+    def __init__(self, x, r, z, p, rz, hist, bnorm):
+        self.x, self.r, self.z, self.p, self.rz = x, r, z, p, rz
+        self.hist = hist
+        self.bnorm = bnorm
+        self.k = len(hist) - 1
+        self.stop = None
+
+
+def pcg_start(A, b, x0, Dinv):
+    r = b - A @ x0
+    z = apply_block(Dinv, r)
+    return PCGState(x0.copy(), r, z, z.copy(), float(r @ z), [float(np.linalg.norm(r))],
+                    float(np.linalg.norm(b)))
+
+
+def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
+    """Run PCG iterations on st until a stop condition or until st.k reaches max_iters."""
+    while True:
+        rn = st.hist[-1]
+        if not np.isfinite(rn):
+            st.stop = STOP_NAN
+            return st
+        if rn <= tol * st.bnorm:
+            st.stop = STOP_CONVERGED
+            return st
+        k = st.k
+        if k >= window:
+            recent = min(st.hist[k - window + 1:k + 1])
+            older = min(st.hist[:k - window + 1])
+            if recent >= older:
+                st.stop = STOP_STAGNATED
+                return st
+        if k >= max_iters:
+            st.stop = STOP_CAP
+            return st
+        q = A @ st.p
+        pq = float(st.p @ q)
+        alpha = st.rz / pq
+        st.x = st.x + alpha * st.p
+        st.r = st.r - alpha * q
+        st.z = apply_block(Dinv, st.r)
+        rz_new = float(st.r @ st.z)
+        beta = rz_new / st.rz
+        st.rz = rz_new
+        st.p = st.z + beta * st.p
+        st.hist.append(float(np.linalg.norm(st.r)))
+        st.k += 1
+
+
+def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000):
+    st = pcg_start(A, b, x0, Dinv)
+    return pcg_run(A, Dinv, st, tol, window, max_iters)
+
+
+def warm_start(A, b, groups, Dinv, fixed, tol=1e-2, max_iters=100):
+    """Per-group independent block-Jacobi PCG on A_GG with zero guess (Q20).
+    groups: (N,) int group id per node (ignored for fixed nodes).  Returns (x0, iters per group)."""
+    N = len(groups)
+    x0 = np.zeros(3 * N)
+    iters = {}
+    free = ~fixed
+    for g in np.unique(groups[free]):
+        nodes = np.nonzero(free & (groups == g))[0]
+        dofs = (3 * nodes[:, None] + np.arange(3)[None]).ravel()
+        Agg = A[dofs][:, dofs]
+        bg = b[dofs]
+        st = PCGState(np.zeros(len(dofs)), bg.copy(), None, None, 0.0, [float(np.linalg.norm(bg))],
+                      float(np.linalg.norm(bg)))
+        Dg = Dinv[nodes]
+        st.z = apply_block(Dg, st.r)
+        st.p = st.z.copy()
+        st.rz = float(st.r @ st.z)
+        it = 0
+        while True:
+            if st.hist[-1] <= tol * st.bnorm or it >= max_iters or not np.isfinite(st.hist[-1]):
+                break
+            q = Agg @ st.p
+            alpha = st.rz / float(st.p @ q)
+            st.x = st.x + alpha * st.p
+            st.r = st.r - alpha * q
+            st.z = apply_block(Dg, st.r)
+            rz_new = float(st.r @ st.z)
+            beta = rz_new / st.rz
+            st.rz = rz_new
+            st.p = st.z + beta * st.p
+            st.hist.append(float(np.linalg.norm(st.r)))
+            it += 1
+        x0[dofs] = st.x
+        iters[int(g)] = it
+    return x0, iters

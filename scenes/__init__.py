@@ -1,0 +1,258 @@
+"""Seeded synthetic scene generators.
+
+This module is the ONLY code shared by the CPU oracle (``oracle/``) and the
+CUDA path (``paper_2407_00046_b200/``).  It holds none of the method's
+arithmetic: it only lays out tetrahedral meshes, fixed-node flags, materials,
+initial positions/velocities and scene parameters, drawing every random number
+from ``numpy.random.default_rng(seed)`` in a fixed order.  Surface extraction,
+masses, Lamé parameters, energies etc. are computed independently by each side.
+
+Scene defaults follow Table 1 of the paper: nu = 0.4,
+rho = 1e3 kg/m^3, dhat = eps_v = 1e-3, h = 1/30 s; gravity (0, -9.81, 0)
+(SURVEY Q4 reading).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+DEFAULT_PARAMS = dict(
+    h=1.0 / 30.0,
+    gravity=(0.0, -9.81, 0.0),
+    dhat=1e-3,
+    eps_v=1e-3,
+    chi=0.0,
+    newton_rel_tol=1e-4,   # Alg. 1 line 9
+    pcg_rel_tol=1e-4,      # App. B
+    pcg_stall_window=100,  # App. B
+    pcg_resume_iters=100,  # App. B
+    alpha_min=1e-9,        # App. B
+    ws_rel_tol=1e-2,
+    ws_max_iters=100,
+    max_newton=1000,
+    max_pcg=20000,
+    max_constraints=1 << 26,
+)
+
+
+# --------------------------------------------------------------------------
+# primitive builders
+# --------------------------------------------------------------------------
+def _kuhn_tets(v):
+    """6-tet Kuhn split of a hex whose 8 corner ids are v[(i,j,k)] (bits x,y,z)."""
+    perms = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+    out = []
+    for a, b, _c in perms:
+        p0 = (0, 0, 0)
+        p1 = [0, 0, 0]
+        p1[a] = 1
+        p2 = list(p1)
+        p2[b] = 1
+        out.append([v[p0], v[tuple(p1)], v[tuple(p2)], v[(1, 1, 1)]])
+    return out
+
+
+def _orient(x, tets):
+    """Swap two vertices of every tet with negative signed volume."""
+    a, b, c, d = (x[tets[:, i]] for i in range(4))
+    vol = np.einsum("ij,ij->i", np.cross(b - a, c - a), d - a)
+    neg = vol < 0
+    t = tets.copy()
+    t[neg, 2], t[neg, 3] = tets[neg, 3], tets[neg, 2]
+    return t
+
+
+def hex_block(nx, ny, nz, size):
+    """Structured hex grid of nx*ny*nz cells over [0,size]^3 (anisotropic if size is a 3-tuple),
+    each cell split into 6 Kuhn tets.  Returns (x (N,3), tets (T,4))."""
+    size = np.broadcast_to(np.asarray(size, dtype=np.float64), (3,))
+    gx = np.linspace(0.0, size[0], nx + 1)
+    gy = np.linspace(0.0, size[1], ny + 1)
+    gz = np.linspace(0.0, size[2], nz + 1)
+    X, Y, Z = np.meshgrid(gx, gy, gz, indexing="ij")
+    x = np.stack([X.ravel(), Y.ravel(), Z.ravel()], axis=1)
+
+    def nid(i, j, k):
+        return (i * (ny + 1) + j) * (nz + 1) + k
+
+    tets = []
+    for i in range(nx):
+        for j in range(ny):
+            for k in range(nz):
+                v = {}
+                for di in (0, 1):
+                    for dj in (0, 1):
+                        for dk in (0, 1):
+                            v[(di, dj, dk)] = nid(i + di, j + dj, k + dk)
+                tets.extend(_kuhn_tets(v))
+    tets = np.asarray(tets, dtype=np.int64)
+    return x, _orient(x, tets)
+
+
+def voxel_mesh(occ, voxel):
+    """Tet mesh of the occupied voxels of a boolean grid occ[nx,ny,nz] (6 Kuhn tets per voxel),
+    with shared corner nodes deduplicated.  Returns (x (N,3), tets (T,4))."""
+    occ = np.asarray(occ, dtype=bool)
+    nx, ny, nz = occ.shape
+    idx = np.argwhere(occ)
+    if len(idx) == 0:
+        return np.zeros((0, 3)), np.zeros((0, 4), dtype=np.int64)
+    corner_offsets = np.array([(di, dj, dk) for di in (0, 1) for dj in (0, 1) for dk in (0, 1)])
+    corners = (idx[:, None, :] + corner_offsets[None, :, :]).reshape(-1, 3)
+    lin = (corners[:, 0] * (ny + 1) + corners[:, 1]) * (nz + 1) + corners[:, 2]
+    uniq, inv = np.unique(lin, return_inverse=True)
+    inv = inv.reshape(-1, 8)
+    ci = uniq // ((ny + 1) * (nz + 1))
+    cj = (uniq // (nz + 1)) % (ny + 1)
+    ck = uniq % (nz + 1)
+    x = np.stack([ci, cj, ck], axis=1).astype(np.float64) * voxel
+    # Kuhn split with vectorised corner lookup
+    code = {tuple(o): n for n, o in enumerate(corner_offsets)}
+    perms = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+    tl = []
+    for a, b, _c in perms:
+        p1 = [0, 0, 0]
+        p1[a] = 1
+        p2 = list(p1)
+        p2[b] = 1
+        tl.append(np.stack([inv[:, code[(0, 0, 0)]], inv[:, code[tuple(p1)]],
+                            inv[:, code[tuple(p2)]], inv[:, code[(1, 1, 1)]]], axis=1))
+    tets = np.stack(tl, axis=1).reshape(-1, 4).astype(np.int64)
+    return x, _orient(x, tets)
+
+
+def rot_y(theta):
+    c, s = np.cos(theta), np.sin(theta)
+    return np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+
+
+def rot_axis(axis, theta):
+    axis = np.asarray(axis, dtype=np.float64)
+    axis = axis / np.linalg.norm(axis)
+    K = np.array([[0, -axis[2], axis[1]], [axis[2], 0, -axis[0]], [-axis[1], axis[0], 0]])
+    return np.eye(3) + np.sin(theta) * K + (1 - np.cos(theta)) * (K @ K)
+
+
+def random_rotation(rng):
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    return np.array([
+        [1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+        [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+        [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)],
+    ])
+
+
+class SceneBuilder:
+    """Accumulates bodies (tet meshes), fixed obstacle triangles and per-node velocities."""
+
+    def __init__(self):
+        self.x = []
+        self.tets = []
+        self.mat = []
+        self.fixed = []
+        self.v = []
+        self.obst_tris = []
+        self.n = 0
+
+    def add_body(self, x, tets, material, v0=(0.0, 0.0, 0.0), fixed=None):
+        x = np.asarray(x, dtype=np.float64)
+        self.x.append(x)
+        self.tets.append(np.asarray(tets, dtype=np.int64) + self.n)
+        self.mat.append(np.full(len(tets), material, dtype=np.int32))
+        f = np.zeros(len(x), dtype=np.uint8) if fixed is None else np.asarray(fixed, dtype=np.uint8)
+        self.fixed.append(f)
+        self.v.append(np.broadcast_to(np.asarray(v0, dtype=np.float64), x.shape).copy())
+        self.n += len(x)
+
+    def add_obstacle(self, x, tris):
+        """Surface-only static obstacle: nodes are fixed, triangles are listed explicitly."""
+        x = np.asarray(x, dtype=np.float64)
+        self.x.append(x)
+        self.fixed.append(np.ones(len(x), dtype=np.uint8))
+        self.v.append(np.zeros_like(x))
+        self.obst_tris.append(np.asarray(tris, dtype=np.int64) + self.n)
+        self.n += len(x)
+
+    def build(self, materials, name, **params):
+        p = dict(DEFAULT_PARAMS)
+        p.update(params)
+        x = np.concatenate(self.x, axis=0)
+        tets = np.concatenate(self.tets, axis=0) if self.tets else np.zeros((0, 4), np.int64)
+        return dict(
+            name=name,
+            rest_x=x.copy(),
+            x0=x.copy(),
+            v0=np.concatenate(self.v, axis=0),
+            tets=tets.astype(np.int32),
+            tet_material=(np.concatenate(self.mat) if self.mat else np.zeros(0, np.int32)).astype(np.int32),
+            node_fixed=np.concatenate(self.fixed).astype(np.uint8),
+            obstacle_tris=(np.concatenate(self.obst_tris, axis=0) if self.obst_tris
+                           else np.zeros((0, 3), np.int64)).astype(np.int32),
+            materials=np.asarray(materials, dtype=np.float64).reshape(-1, 3),  # (E, nu, rho)
+            params=p,
+        )
+
+
+def _plane(half, y=0.0, cx=0.0, cz=0.0):
+    """Two triangles at height y, normal +y (counter-clockwise seen from above)."""
+    x = np.array([[cx - half, y, cz - half], [cx + half, y, cz - half],
+                  [cx + half, y, cz + half], [cx - half, y, cz + half]])
+    tris = np.array([[0, 2, 1], [0, 3, 2]])
+    return x, tris
+
+
+# --------------------------------------------------------------------------
+# C1: two stacked soft cubes dropped on a plane (BASELINE.json configs[0])
+# --------------------------------------------------------------------------
+def make_cubes(seed=1, cells=5, edge=1.0, E=1e5, nu=0.4, rho=1e3, gap=0.01, speed=1.0):
+    """C1 recipe: 2 cubes of 5x5x5 hex cells (Kuhn split, T=1500),
+    yaws ~U(10,35) deg, top tilt ~U(0.5,2) deg about a random horizontal axis; bottom base at
+    y = gap, top cube `gap` above; v0 = (0,-speed,0); static 10x10 m plane (2 tris) at y = 0."""
+    rng = np.random.default_rng(seed)
+    yaw0 = np.deg2rad(rng.uniform(10.0, 35.0))
+    yaw1 = np.deg2rad(rng.uniform(10.0, 35.0))
+    tilt = np.deg2rad(rng.uniform(0.5, 2.0))
+    phi = rng.uniform(0.0, 2 * np.pi)
+    axis = np.array([np.cos(phi), 0.0, np.sin(phi)])
+
+    xb, tb = hex_block(cells, cells, cells, edge)
+    c = np.array([edge / 2, edge / 2, edge / 2])
+    sb = SceneBuilder()
+    # bottom cube
+    x0 = (xb - c) @ rot_y(yaw0).T
+    x0[:, 1] += -x0[:, 1].min() + gap
+    # top cube
+    R1 = rot_axis(axis, tilt) @ rot_y(yaw1)
+    x1 = (xb - c) @ R1.T
+    x1[:, 1] += -x1[:, 1].min() + x0[:, 1].max() + gap
+    sb.add_body(x0, tb, 0, v0=(0.0, -speed, 0.0))
+    sb.add_body(x1, tb, 0, v0=(0.0, -speed, 0.0))
+    px, pt = _plane(5.0)
+    sb.add_obstacle(px, pt)
+    return sb.build([(E, nu, rho)], "C1-cubes", chi=0.0)
+
+
+def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0):
+    """Tiny fixture: one generically rotated tet above a plane."""
+    rng = np.random.default_rng(seed)
+    x = np.array([[0, 0, 0], [0.1, 0, 0], [0, 0.1, 0], [0, 0, 0.1]], dtype=np.float64)
+    x = (x - x.mean(0)) @ random_rotation(rng).T
+    x[:, 1] += -x[:, 1].min() + height
+    tets = _orient(x, np.array([[0, 1, 2, 3]]))
+    sb = SceneBuilder()
+    sb.add_body(x, tets, 0, v0=(0.0, -speed, 0.0))
+    px, pt = _plane(1.0)
+    sb.add_obstacle(px, pt)
+    return sb.build([(E, nu, rho)], "tet")
+
+
+def perturbed(scene, seed, scale):
+    """Copy of `scene` with x0 randomly perturbed (free nodes only) by N(0, scale^2)."""
+    rng = np.random.default_rng(seed)
+    s = dict(scene)
+    x = scene["x0"].copy()
+    free = scene["node_fixed"] == 0
+    x[free] += rng.normal(scale=scale, size=(free.sum(), 3))
+    s["x0"] = x
+    return s
