@@ -25,6 +25,7 @@ from . import ccd as ccdm
 from . import contact as cm
 from . import linalg as la
 from .assemble import floor_log10
+from .auglag import aprime_rule, dual_update, sigma_ls, sigma_schedule, slack
 from .energy import barrier, inertia_energy, inertia_grad, nh_energy, nh_stencils
 from .mesh import precompute
 from .projection import project_eigh
@@ -203,10 +204,8 @@ class Oracle:
         gE[fd] = 0.0
         gb[fd] = 0.0
         floor = float(np.mean(m.mass[self.free])) / (self.h * self.h)
-        bb = float(gb @ gb)
-        if bb == 0.0:
-            return floor
-        return max(-float(gb @ gE) / bb, floor)
+        s_ls = sigma_ls(gb, gE)
+        return floor if s_ls is None else max(s_ls, floor)
 
     # ---------------------------------------------------------------------- step
     def step(self, x_t, v_t, trace=None):
@@ -235,11 +234,10 @@ class Oracle:
             keys, d = cm.constraint_set(x, pt, ee, dhat)
             dmin = float(d.min()) if len(d) else np.inf
             rebuilt = False
-            if self.flags & FLAG_NO_AUGLAG:
-                pass
-            elif dmin > 1e-2 * dhat:
+            rule = "keep" if self.flags & FLAG_NO_AUGLAG else aprime_rule(dmin, dmin_prev, len(st["ap_keys"]) == 0, dhat)
+            if rule == "clear":
                 st["ap_keys"], st["ap_mu"], st["ap_s"] = np.zeros((0, 5), np.int64), np.zeros(0), np.zeros(0)
-            elif dmin < dmin_prev or len(st["ap_keys"]) == 0:
+            elif rule == "rebuild":
                 newk = keys[d < 1e-2 * dhat]
                 mu_new, s_new = np.zeros(len(newk)), np.zeros(len(newk))
                 old = {tuple(k): (mu_, s_) for k, mu_, s_ in zip(st["ap_keys"], st["ap_mu"], st["ap_s"])}
@@ -317,14 +315,13 @@ class Oracle:
             # AL updates on A' (lines 12-14)
             if len(st["ap_keys"]):
                 dn = cm.key_distance(x_new, st["ap_keys"])
-                s_new = np.maximum(-st["ap_mu"] / st["sigma"] - dhat + dn, 0.0)
+                s_new = slack(st["ap_mu"], st["sigma"], dhat, dn)
                 st["ap_s"] = s_new
-                st["ap_mu"] = st["ap_mu"] + st["sigma"] * barrier(dn, dhat + s_new)
+                st["ap_mu"] = dual_update(st["ap_mu"], st["sigma"], dhat, s_new, dn)
             # sigma schedule (lines 15-16)
             if not (self.flags & FLAG_NO_AUGLAG):
                 _k2, d2 = cm.constraint_set(x_new, cpt, cee, dhat)
-                if len(d2) and float(d2.min()) < 1e-2 * dhat:
-                    st["sigma"] = max(1.2 * st["sigma"], 100.0 * sig0)
+                st["sigma"] = sigma_schedule(st["sigma"], sig0, float(d2.min()) if len(d2) else np.inf, dhat)
             x = x_new
         if not converged:
             raise NotConverged("Newton iteration cap reached")

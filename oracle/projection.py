@@ -37,7 +37,7 @@ def project_jacobi(H, tol=1e-15, max_sweeps=100):
     V = np.eye(n)
     fro = np.linalg.norm(A)
     for _ in range(max_sweeps):
-        off = np.sqrt(max(np.sum(A * A) - np.sum(np.diag(A) ** 2), 0.0))
+        off = np.sqrt(np.sum((A - np.diag(np.diag(A))) ** 2))
         if off <= tol * fro:
             break
         for p in range(n - 1):

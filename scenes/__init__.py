@@ -256,3 +256,26 @@ def perturbed(scene, seed, scale):
     x[free] += rng.normal(scale=scale, size=(free.sum(), 3))
     s["x0"] = x
     return s
+
+
+def make_two_tets(seed=0, gap=0.004, speed=0.3, E=1e5, nu=0.4, rho=1e3):
+    """Gravity-free, frictionless, obstacle-free two-tet collision (momentum test, SURVEY c.3)."""
+    rng = np.random.default_rng(seed)
+    base = np.array([[0, 0, 0], [0.1, 0, 0], [0, 0.1, 0], [0, 0, 0.1]], dtype=np.float64)
+    xa = (base - base.mean(0)) @ random_rotation(rng).T
+    xb = (base - base.mean(0)) @ random_rotation(rng).T
+    xb[:, 0] += xa[:, 0].max() - xb[:, 0].min() + gap
+    sb = SceneBuilder()
+    sb.add_body(xa, _orient(xa, np.array([[0, 1, 2, 3]])), 0, v0=(speed, 0.0, 0.0))
+    sb.add_body(xb, _orient(xb, np.array([[0, 1, 2, 3]])), 0, v0=(-speed, 0.0, 0.0))
+    return sb.build([(E, nu, rho)], "two-tets", gravity=(0.0, 0.0, 0.0))
+
+
+def make_free_cube(seed=0, cells=3, E=1e5, nu=0.4, rho=1e3):
+    """One rest-shape cube in free fall, no obstacles (free-fall test, SURVEY c.3)."""
+    rng = np.random.default_rng(seed)
+    xb, tb = hex_block(cells, cells, cells, 0.5)
+    xb = (xb - 0.25) @ random_rotation(rng).T
+    sb = SceneBuilder()
+    sb.add_body(xb, tb, 0, v0=tuple(rng.normal(size=3)))
+    return sb.build([(E, nu, rho)], "free-cube")

@@ -1,0 +1,185 @@
+"""Pins of the oracle's projection, assembly, stiffness groups, SpMV, PCG and warm start
+(SURVEY.md §8(c) c.3).  CPU only."""
+import numpy as np
+import pytest
+
+import scenes
+from oracle import linalg as la
+from oracle.assemble import BlockSystem, floor_log10, stiffness_groups
+from oracle.bal import Oracle
+from oracle.projection import lambda_bar, project_eigh, project_jacobi
+
+
+# ---------------------------------------------------------------- projection (Q21)
+def test_projection_properties():
+    rng = np.random.default_rng(20)
+    for n in (6, 9, 12):
+        A = rng.normal(size=(n, n))
+        H = A + A.T
+        P, wc = project_eigh(H[None])
+        P = P[0]
+        assert np.array_equal(P, P.T)
+        assert np.linalg.eigvalsh(P).min() >= -1e-14 * np.linalg.norm(H)
+        P2, _ = project_eigh(P[None])  # idempotent
+        assert np.linalg.norm(P2[0] - P) <= 1e-13 * np.linalg.norm(H)
+        Pj, _ = project_jacobi(H)       # unique nearest PSD matrix: any correct eigensolver agrees
+        assert np.linalg.norm(Pj - P) <= 1e-13 * np.linalg.norm(H)
+        # Frobenius-nearest: no random PSD matrix is closer
+        for _ in range(20):
+            B = rng.normal(size=(n, n))
+            Q = P + 1e-3 * (B @ B.T)
+            assert np.linalg.norm(H - Q) >= np.linalg.norm(H - P)
+        assert lambda_bar(P[None])[0] == pytest.approx(np.mean(wc[0]), rel=1e-12)
+        # PSD input unchanged
+        S = A @ A.T
+        Ps, _ = project_eigh(S[None])
+        assert np.linalg.norm(Ps[0] - S) <= 1e-13 * np.linalg.norm(S)
+
+
+# ---------------------------------------------------------------- groups (Q17-Q19)
+def test_floor_log10_exact_decades():
+    e = np.array([1.0, 9.999999999999999, 10.0, 1e4, 30003.0, 1e-3, 0.00099999999, 1e12 * (1 - 1e-16)])
+    assert list(floor_log10(e)) == [0, 0, 1, 4, 4, -3, -4, 11]
+
+
+def test_stiffness_group_examples():
+    # one stencil over nodes 0-3 with lambda_bar = 1e4, m/h^2 = 1 -> e = 3(1e4 + 1) = 30003 -> group 4
+    mass = np.ones(8)
+    e, g = stiffness_groups(mass, 1.0, [np.array([0, 1, 2, 3])], [1e4], np.zeros(8, bool))
+    assert e[0] == pytest.approx(30003.0) and g[0] == 4
+    # two disjoint stencils 1e4 and 1e6 -> groups {4, 6}
+    e, g = stiffness_groups(mass, 1.0, [np.array([0, 1, 2, 3]), np.array([4, 5, 6, 7])], [1e4, 1e6],
+                            np.zeros(8, bool))
+    assert set(g[:4]) == {4} and set(g[4:]) == {6}
+
+
+# ---------------------------------------------------------------- assembly vs dense brute force
+def _dense_brute(o, x, asm):
+    """Sum_i S_i^T P(H_i) S_i + M/h^2 with explicit dense selection matrices (N small)."""
+    m = o.mesh
+    N = o.N
+    A = np.diag(np.repeat(m.mass / o.h ** 2, 3))
+    for e, tet in enumerate(m.tets):
+        S = np.zeros((12, 3 * N))
+        for a, n in enumerate(tet):
+            S[3 * a:3 * a + 3, 3 * n:3 * n + 3] = np.eye(3)
+        A += S.T @ asm["elastic_P"][e] @ S
+    for key, P in zip(asm["contact_keys"], asm["contact_P"]):
+        ids = [i for i in key[1:] if i >= 0]
+        S = np.zeros((3 * len(ids), 3 * N))
+        for a, n in enumerate(ids):
+            S[3 * a:3 * a + 3, 3 * n:3 * n + 3] = np.eye(3)
+        A += S.T @ P @ S
+    fd = np.repeat(m.fixed, 3)
+    A[fd, :] = 0
+    A[:, fd] = 0
+    A[fd, fd] = 1.0
+    return A
+
+
+def test_assembly_matches_dense_and_is_spd():
+    sc = scenes.make_single_tet(0, height=0.0004)  # within dhat of the plane: contact stencils too
+    o = Oracle(sc)
+    x = sc["x0"] + 1e-4 * np.random.default_rng(21).normal(size=sc["x0"].shape) * (~o.mesh.fixed[:, None])
+    from oracle import contact as cm
+    pt, ee = cm.candidates(o.mesh, x, x, o.dhat)
+    keys, d = cm.constraint_set(x, pt, ee, o.dhat)
+    assert len(keys) > 0
+    st = dict(y=x.copy(), x_t=x.copy(), sigma=1e3, ap_keys=np.zeros((0, 5), np.int64), ap_mu=np.zeros(0),
+              ap_s=np.zeros(0), fr_keys=None)
+    asm = o.assemble(x, st, keys)
+    A = asm["A"].toarray()
+    Ad = _dense_brute(o, x, asm)
+    assert np.linalg.norm(A - Ad) <= 1e-13 * np.linalg.norm(Ad)
+    assert np.allclose(A, A.T, rtol=0, atol=1e-12 * np.abs(A).max())
+    assert np.linalg.eigvalsh(A).min() > 0
+
+
+def test_elastic_rows_annihilate_translations(cubes):
+    o = Oracle(cubes)
+    rng = np.random.default_rng(22)
+    x = cubes["x0"] + 0.01 * rng.normal(size=cubes["x0"].shape) * (~o.mesh.fixed[:, None])
+    from oracle.energy import nh_stencils
+    from oracle.projection import project_eigh as pe
+    _v, _g, H = nh_stencils(x, o.mesh)
+    P, _ = pe(H)
+    for c in range(3):
+        t = np.zeros(12)
+        t[c::3] = 1.0
+        assert np.max(np.linalg.norm(P @ t, axis=1)) <= 1e-10 * np.max(np.linalg.norm(P, axis=(1, 2)))
+
+
+# ---------------------------------------------------------------- SpMV / PCG / warm start
+def _rand_spd_blocks(rng, N, density=0.3, cond_scale=1.0):
+    bs = BlockSystem(N)
+    for i in range(N):
+        for j in range(i):
+            if rng.uniform() < density:
+                B = rng.normal(size=(3, 3)) * 0.3
+                bs.add(i, j, B)
+                bs.add(j, i, B.T)
+    A = bs.to_dense()
+    lam = np.linalg.eigvalsh(A).min()
+    for i in range(N):
+        bs.add(i, i, (abs(lam) + 1.0) * np.eye(3) * cond_scale ** rng.uniform(0, 1))
+    return bs
+
+
+def test_spmv_is_dense_product_and_symmetric():
+    rng = np.random.default_rng(23)
+    bs = _rand_spd_blocks(rng, 30)
+    A = bs.to_csr()
+    Ad = bs.to_dense()
+    v, w = rng.normal(size=90), rng.normal(size=90)
+    np.testing.assert_allclose(A @ v, Ad @ v, rtol=1e-13, atol=1e-13 * np.abs(Ad).max())
+    assert float(v @ (A @ w)) == pytest.approx(float(w @ (A @ v)), rel=1e-12)
+
+
+def test_pcg_special_cases_and_dense_solve():
+    rng = np.random.default_rng(24)
+    import scipy.sparse as sp
+    # identity -> 1 iteration
+    N = 10
+    Dinv = np.tile(np.eye(3), (N, 1, 1))
+    b = rng.normal(size=3 * N)
+    st = la.pcg(sp.identity(3 * N, format="csr"), b, np.zeros(3 * N), Dinv, tol=1e-12)
+    assert st.k == 1 and np.allclose(st.x, b)
+    # diagonal with 3 distinct eigenvalues, identity preconditioner -> <= 3 iterations
+    dg = np.repeat([1.0, 2.0, 3.0], N)
+    A = sp.diags(dg).tocsr()
+    st = la.pcg(A, b, np.zeros(3 * N), Dinv, tol=1e-12)
+    assert st.k <= 3 and np.allclose(st.x, b / dg, rtol=1e-10)
+    # random SPD vs dense solve
+    bs = _rand_spd_blocks(rng, 25, cond_scale=1e3)
+    A = bs.to_csr()
+    Dinv = np.linalg.inv(bs.diag_blocks())
+    b = rng.normal(size=75)
+    st = la.pcg(A, b, np.zeros(75), Dinv, tol=1e-13, window=10 ** 9)
+    xd = np.linalg.solve(bs.to_dense(), b)
+    assert np.linalg.norm(st.x - xd) <= 1e-9 * np.linalg.norm(xd)
+    # App. B stagnation: a stalled residual history stops the solve
+    s2 = la.PCGState(np.zeros(3), np.ones(3), np.ones(3), np.ones(3), 1.0, [1.0] * 101, 1.0)
+    la.pcg_run(sp.identity(3, format="csr"), np.tile(np.eye(3), (1, 1, 1)), s2, 1e-4, 100, 10 ** 6)
+    assert s2.stop == la.STOP_STAGNATED
+
+
+def test_warm_start_exact_on_decoupled_groups():
+    rng = np.random.default_rng(25)
+    b1 = _rand_spd_blocks(rng, 8)
+    b2 = _rand_spd_blocks(rng, 6)
+    bs = BlockSystem(14)
+    for (i, j), B in b1.blocks.items():
+        bs.add(i, j, B)
+    for (i, j), B in b2.blocks.items():
+        bs.add(i + 8, j + 8, 1e4 * B)
+    A = bs.to_csr()
+    Dinv = np.linalg.inv(bs.diag_blocks())
+    groups = np.array([2] * 8 + [6] * 6)
+    b = rng.normal(size=42)
+    x0, it = la.warm_start(A, b, groups, Dinv, np.zeros(14, bool), tol=1e-14, max_iters=1000)
+    xd = np.linalg.solve(bs.to_dense(), b)
+    assert np.linalg.norm(x0 - xd) <= 1e-11 * np.linalg.norm(xd)
+    st = la.pcg(A, b, x0, Dinv, tol=1e-10)
+    assert st.k <= 1
+    x0z, _ = la.warm_start(A, np.zeros(42), groups, Dinv, np.zeros(14, bool))
+    assert np.all(x0z == 0)
