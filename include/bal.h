@@ -1,0 +1,233 @@
+/*
+ * bal.h -- C ABI of libbal.so: the B200-native BAL inexact Newton-PCG hot path of
+ * "Barrier-Augmented Lagrangian for GPU-based Elastodynamic Contact" (arXiv 2407.00046).
+ *
+ * Citations: P:n = PAPER.md line n (section / equation given), Qn = SURVEY.md §8(c) reading n,
+ * R-xxx = DESIGN.md reading.
+ *
+ * General conventions (apply to every entry point):
+ *  - Every function returns bal_status (0 = OK, < 0 = error) and never aborts or exits; the
+ *    human-readable reason of the last failure is available from bal_last_error(ctx).
+ *  - Ownership: every array passed in or out is caller-owned; no pointer is retained across
+ *    calls.  bal_init copies what it needs (host arrays may be freed on return).  The library
+ *    owns all of its device memory and frees it in bal_destroy.
+ *  - Memory space: bal_init takes HOST arrays.  Per-step arrays are DEVICE pointers on the
+ *    ctx's device (e.g. torch.Tensor.data_ptr() of a contiguous float64 CUDA tensor) unless a
+ *    function says otherwise.  bal_step_host is the end-to-end variant taking HOST arrays.
+ *  - Layout: positions / velocities / vectors are AoS xyz per node, float64[3*n_nodes].
+ *  - Precision: FP64 throughout ("We use double precision as default").
+ *  - Synchronisation: calls are stream-ordered on the ctx stream (bal_set_stream); every call
+ *    returns with its results complete on that stream.
+ *  - Threads: a ctx is not thread-safe; distinct ctxs are independent.
+ */
+#ifndef BAL_H
+#define BAL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bal_ctx bal_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  BAL_OK = 0,
+  BAL_E_INVALID_ARG = -1,     /* NULL / out-of-range argument */
+  BAL_E_BAD_MESH = -2,        /* inverted or degenerate rest tet, bad index */
+  BAL_E_INFEASIBLE = -3,      /* input has a surface distance <= 0 or a tet with J <= 0 */
+  BAL_E_NOT_CONVERGED = -4,   /* Newton cap or line-search failure; x_next = last accepted iterate */
+  BAL_E_CONSTRAINT_BUDGET = -5,
+  BAL_E_CUDA = -6,
+  BAL_E_NCCL = -7,
+  BAL_E_OOM = -8,
+  BAL_E_NAN = -9
+} bal_status;
+
+/* Tetrahedral mesh (host arrays).  P:134-146 (§3.1): nodal positions, lumped mass from rho. */
+typedef struct {
+  int32_t n_nodes, n_tets;
+  const double* rest_x;          /* [3*n_nodes] rest positions */
+  const int32_t* tets;           /* [4*n_tets], positive orientation (det D_m > 0) */
+  const uint8_t* node_fixed;     /* [n_nodes] 1 = static obstacle / Dirichlet node (App. C) */
+  const int32_t* tet_material;   /* [n_tets] index into the materials array */
+  int32_t n_obstacle_tris;       /* surface-only static obstacles */
+  const int32_t* obstacle_tris;  /* [3*n_obstacle_tris]; every referenced node must be fixed */
+} bal_mesh;
+
+/* Neo-Hookean material (Q1: Psi = mu/2 (tr F^T F - 3) - mu ln J + lam/2 (ln J)^2). */
+typedef struct { double E, nu, rho; } bal_material;
+
+/* Flags */
+#define BAL_NO_WARMSTART 1u  /* ablation: global PCG from x0 = 0 */
+#define BAL_NO_AUGLAG 2u     /* ablation: A' = {} and sigma = sigma0 (plain IPC barrier Newton) */
+
+/* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
+typedef struct {
+  double h;              /* time step (s) */
+  double gravity[3];     /* m/s^2 (Q4) */
+  double dhat;           /* collision offset */
+  double eps_v;          /* friction mollifier threshold */
+  double chi;            /* friction coefficient */
+  double newton_rel_tol; /* 1e-4, Alg. 1 line 9 */
+  double pcg_rel_tol;    /* 1e-4, App. B */
+  int32_t pcg_stall_window; /* 100, App. B */
+  int32_t pcg_resume_iters; /* 100, App. B */
+  double alpha_min;      /* 1e-9, App. B */
+  double ws_rel_tol;     /* 1e-2 (Q20) */
+  int32_t ws_max_iters;  /* 100 (Q20) */
+  int32_t max_newton;    /* 1000 (Q13) */
+  int32_t max_pcg;       /* 20000 (Q16) */
+  int64_t max_constraints; /* constraint budget, P:440 (Q36) */
+  uint32_t flags;        /* BAL_NO_WARMSTART | BAL_NO_AUGLAG */
+} bal_params;
+
+/* Per-step statistics (Table 1 columns "avg. #iters (Newton)", "#cons"). */
+typedef struct {
+  int32_t newton_iters;
+  int64_t pcg_iters;       /* global PCG iterations summed over Newton iterations */
+  int64_t ws_iters;        /* warm-start iterations (max over groups) summed over Newton iterations */
+  int32_t max_constraints; /* max |A| over Newton iterations */
+  int32_t max_aprime;      /* max |A'| */
+  double sigma0, sigma_final, min_distance, last_rel_grad;
+  double ms_total, ms_collision, ms_assembly, ms_warmstart, ms_pcg, ms_linesearch;
+} bal_step_stats;
+
+/* Create a context: validates the mesh, precomputes D_m^{-1}, volumes, lumped masses,
+ * surface triangles / edges, the static BSR pattern and the atomic-free slot lists, and uploads
+ * everything to `device`.  Errors: BAL_E_INVALID_ARG, BAL_E_BAD_MESH, BAL_E_CUDA, BAL_E_OOM.
+ * On error *out is NULL. */
+bal_status bal_init(const bal_mesh* mesh, const bal_material* materials, int32_t n_materials,
+                    const bal_params* params, int32_t device, bal_ctx** out);
+
+/* Use `cuda_stream` (a cudaStream_t) for all subsequent work; NULL = the ctx's own stream. */
+bal_status bal_set_stream(bal_ctx* ctx, void* cuda_stream);
+
+/* One backward-Euler time step solved by Alg. 1 with the inexact
+ * Newton-PCG primal solve of §4.  x_t, v_t: device [3N]; x_next: device [3N];
+ * v_next: device [3N] or NULL (v_{t+1} = (x_{t+1}-x_t)/h, eq:int:x).  stats may be NULL.
+ * Errors: BAL_E_INFEASIBLE (input distance <= 0), BAL_E_NOT_CONVERGED (x_next = last accepted
+ * iterate, still intersection-free), BAL_E_NAN, BAL_E_CUDA, BAL_E_OOM. */
+bal_status bal_step(bal_ctx* ctx, const double* x_t, const double* v_t, double* x_next,
+                    double* v_next, bal_step_stats* stats);
+
+/* End-to-end variant of bal_step: x_t, v_t, x_next, v_next are HOST arrays [3N]; the
+ * host<->device copies are part of the call (used for the e2e measurement). */
+bal_status bal_step_host(bal_ctx* ctx, const double* x_t, const double* v_t, double* x_next,
+                         double* v_next, bal_step_stats* stats);
+
+/* ----------------------------------------------------------------------------------------
+ * Testing surface.  Same device-pointer conventions.
+ * --------------------------------------------------------------------------------------*/
+
+/* Contact state for bal_assemble: keys of the active set A and of the augmentation set A'
+ * (key = [type, n0, n1, n2, n3], type 0=PP 1=PE 2=PT 3=EE, canonical node order, -1 padding;
+ * Q10, Q27, Q28) with the multipliers mu and slacks s of A', penalty sigma, and the
+ * friction anchors (lambda, Gamma, n) of the friction pairs (Q25, Q26).
+ * All arrays are HOST arrays. */
+typedef struct {
+  int32_t n_active;
+  const int32_t* active_keys;   /* [5*n_active] */
+  int32_t n_aprime;
+  const int32_t* aprime_keys;   /* [5*n_aprime] */
+  const double* aprime_mu;      /* [n_aprime] */
+  const double* aprime_s;       /* [n_aprime] */
+  double sigma;
+  int32_t n_friction;
+  const int32_t* friction_keys; /* [5*n_friction] */
+  const double* friction_gamma; /* [4*n_friction] signed closest-point weights */
+  const double* friction_n;     /* [3*n_friction] unit normals */
+  const double* friction_lambda;/* [n_friction] normal force magnitudes */
+  const double* x_t;            /* HOST [3N] start-of-step positions (friction), may be NULL */
+  const double* y;              /* HOST [3N] inertial predictor y = x_t + h v_t + h^2 G */
+} bal_contact_state;
+
+/* Device views of the last assembled system (valid until the next call on ctx). */
+typedef struct {
+  int32_t n_nodes;
+  int32_t nnzb_static;          /* static (mesh-adjacency) full BSR, both triangles */
+  const int32_t* static_row_ptr;/* [N+1] */
+  const int32_t* static_col;    /* [nnzb_static] */
+  const double* static_val;     /* [9*nnzb_static] row-major 3x3 blocks */
+  int32_t nnzb_contact;         /* per-iteration contact/friction BSR, both triangles */
+  const int32_t* contact_row_ptr;
+  const int32_t* contact_col;
+  const double* contact_val;
+  const double* diag_inv;       /* [6*N] symmetric inverse of the diagonal blocks (xx xy xz yy yz zz) */
+  const double* grad;           /* [3N] e = grad L, fixed entries zero */
+  const double* e_node;         /* [N] assembled eigenvalue e_j */
+  const int32_t* group;         /* [N] floor(log10 e_j); INT32_MIN for fixed nodes */
+  int32_t n_elastic;            /* per-tet projected stencil Hessians (lower blocks) */
+  const double* elastic_blocks; /* [n_tets][10][9]: blocks (a,b), a>=b, index a(a+1)/2+b */
+  const double* elastic_lbar;   /* [n_tets] tr P(H)/12 */
+  int32_t n_contact_stencils;
+  const double* contact_blocks; /* [n][10][9] */
+  const double* contact_lbar;   /* [n] */
+  const int32_t* contact_stencil_nodes; /* [n][4], -1 padded */
+} bal_system_view;
+
+/* Assemble the Newton system at x (device [3N]) for the given contact state: elastic (K1),
+ * contact (K2) and friction (K3) stencils, PSD projection, atomic-free gather into BSR,
+ * gradient, Lambda / e_j / groups and the block-Jacobi inverse. */
+bal_status bal_assemble(bal_ctx* ctx, const double* x, const bal_contact_state* cs,
+                        bal_system_view* out_view);
+
+/* y = A v on the last assembled (or loaded) system.  v, y: device [3N]. */
+bal_status bal_spmv(bal_ctx* ctx, const double* v, double* y);
+
+typedef struct {
+  int32_t warm_start;   /* 1 = stiffness-grouped block-Jacobi warm start (Q20) */
+  double rel_tol;       /* ||r|| <= rel_tol ||b|| (App. B, Q14) */
+  int32_t stall_window; /* App. B stagnation window (Q15); <= 0 disables */
+  int32_t max_iters;
+  double ws_rel_tol;    /* Q20 */
+  int32_t ws_max_iters; /* Q20 */
+} bal_pcg_opts;
+
+typedef struct {
+  int32_t iters;        /* global PCG iterations */
+  int32_t stop_reason;  /* 0 converged, 1 stagnated, 2 cap, 3 NaN */
+  int32_t ws_iters_max; /* max warm-start iterations over groups */
+  int32_t n_groups;
+  double rel_residual;  /* ||r|| / ||b|| at exit */
+} bal_pcg_stats;
+
+/* Block-Jacobi PCG with the App. B policy on the last assembled (or loaded)
+ * system: solves A x = rhs.  rhs, x_out device [3N]; x0 device [3N] or NULL (= 0 or the warm
+ * start when opts->warm_start).  opts / stats may be NULL (defaults from bal_params). */
+bal_status bal_pcg(bal_ctx* ctx, const double* rhs, const double* x0, double* x_out,
+                   const bal_pcg_opts* opts, bal_pcg_stats* stats);
+
+/* Test-only: replace the current system by a host BSR (full, both triangles, rows sorted by
+ * column) so SpMV / PCG can be checked on an oracle-assembled matrix.  group may be NULL. */
+typedef struct {
+  int32_t n_nodes, nnzb;
+  const int32_t* row_ptr; /* [N+1] */
+  const int32_t* col;     /* [nnzb] */
+  const double* val;      /* [9*nnzb] */
+  const int32_t* group;   /* [N] or NULL */
+} bal_bsr_host;
+bal_status bal_load_bsr(bal_ctx* ctx, const bal_bsr_host* bsr);
+
+/* Timing helper for the benchmark: run `iters` SpMV launches on the current system with CUDA
+ * events on the ctx stream; returns the mean launch duration in microseconds. */
+bal_status bal_bench_spmv(bal_ctx* ctx, int32_t iters, double* mean_us);
+
+/* Decision trace of the last bal_step (SURVEY c.4): one record of BAL_TRACE_FIELDS doubles per
+ * Newton iteration: l, |A|, |A'|, A'-rebuilt, min d, sigma, warm-start iters (max over groups),
+ * PCG iters, PCG stop reason, alpha_CCD, alpha, halvings, resumes, descent-safeguard used,
+ * ||e^l|| / ||e^0||.  `out` is a HOST array of max_records * BAL_TRACE_FIELDS doubles;
+ * returns the number of records written (or a negative bal_status). */
+#define BAL_TRACE_FIELDS 15
+int32_t bal_get_trace(const bal_ctx* ctx, double* out, int32_t max_records);
+
+/* Counters of kernels launched by the library since ctx creation (bench's gpu_launches). */
+int64_t bal_kernel_launches(const bal_ctx* ctx);
+
+const char* bal_last_error(const bal_ctx* ctx);
+void bal_destroy(bal_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BAL_H */

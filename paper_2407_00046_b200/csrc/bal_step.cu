@@ -1,0 +1,596 @@
+// bal_step.cu -- the barrier-augmented Lagrangian time step (Alg. 1) with its inexact
+// Newton-PCG primal solve (§4); host orchestration of the device kernels, mirroring
+// oracle/bal.py step by step.  Only per-Newton-iteration scalars cross
+// to the host (||e||, alpha_CCD, line-search energies, counts).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include <cub/cub.cuh>
+
+#include "bvh.h"
+#include "ctx.h"
+#include "geometry.cuh"
+
+using namespace bal;
+
+struct StepWork {
+  DevBuf<double> x, xn, dir, rhs, trial, gE, gb, v;
+  Candidates cand_prox, cand_sw;
+  ConstraintSet cs_A, cs_trial;
+  CollisionWork cw;
+  // A' (sorted by key): keys5, packed keys, multipliers, slacks, distances
+  DevBuf<int> ap_keys, ap_keys_new;
+  DevBuf<unsigned long long> ap_hi, ap_lo, ap_hi_new, ap_lo_new;
+  DevBuf<double> ap_mu, ap_s, ap_mu_new, ap_s_new, ap_d;
+  int n_ap = 0;
+  DevBuf<double> evals, esc;  // per-item energies, energy scalars
+  DevBuf<int> sel, selcnt;
+  DevBuf<unsigned char> tmp;
+};
+
+void destroy_step_work(bal_ctx* c) {
+  delete c->sw;
+  c->sw = nullptr;
+}
+
+namespace {
+
+__global__ void k_predictor(int n, const double* __restrict__ xt, const double* __restrict__ vt, double h, double gx,
+                            double gy, double gz, const uint8_t* __restrict__ fixed, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double g[3] = {gx, gy, gz};
+  for (int c = 0; c < 3; ++c) {
+    const size_t j = 3 * (size_t)i + c;
+    y[j] = fixed[i] ? xt[j] : xt[j] + h * vt[j] + h * h * g[c];
+  }
+}
+
+__global__ void k_inertia_energy(int n, const double* __restrict__ x, const double* __restrict__ y,
+                                 const double* __restrict__ mass, double inv_2h2, const uint8_t* __restrict__ fixed,
+                                 double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (fixed[i]) {
+    out[i] = 0.0;
+    return;
+  }
+  double s = 0.0;
+  for (int c = 0; c < 3; ++c) {
+    const double d = x[3 * (size_t)i + c] - y[3 * (size_t)i + c];
+    s += d * d;
+  }
+  out[i] = mass[i] * s * inv_2h2;
+}
+
+__global__ void k_flag_lt(int n, const double* __restrict__ d, double thr, int* flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flag[i] = d[i] < thr ? 1 : 0;
+}
+
+__global__ void k_compact_keys(int n, const int* __restrict__ flag, const int* __restrict__ pos,
+                               const int* __restrict__ keys, const unsigned long long* __restrict__ hi,
+                               const unsigned long long* __restrict__ lo, int* okeys, unsigned long long* ohi,
+                               unsigned long long* olo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || !flag[i]) return;
+  const int p = pos[i];
+  for (int a = 0; a < 5; ++a) okeys[5 * (size_t)p + a] = keys[5 * (size_t)i + a];
+  ohi[p] = hi[i];
+  olo[p] = lo[i];
+}
+
+// carry (mu, s) of surviving A' members by key; new members start at 0 (Q10)
+__global__ void k_carry(int n, const unsigned long long* __restrict__ hi, const unsigned long long* __restrict__ lo,
+                        int nold, const unsigned long long* __restrict__ ohi, const unsigned long long* __restrict__ olo,
+                        const double* __restrict__ omu, const double* __restrict__ os, double* mu, double* s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int a = 0, b = nold;
+  const unsigned long long h = hi[i], l = lo[i];
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (ohi[m] < h || (ohi[m] == h && olo[m] < l)) a = m + 1;
+    else b = m;
+  }
+  const bool found = a < nold && ohi[a] == h && olo[a] == l;
+  mu[i] = found ? omu[a] : 0.0;
+  s[i] = found ? os[a] : 0.0;
+}
+
+// slack and multiplier update on A' (Alg. 1 lines 12-14)
+__global__ void k_al_update(int n, const double* __restrict__ d, double sigma, double dhat, double* mu, double* s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double sn = fmax(-mu[i] / sigma - dhat + d[i], 0.0);
+  s[i] = sn;
+  mu[i] = mu[i] + sigma * barrier_b(d[i], dhat + sn);
+}
+
+// friction anchors per stencil of A u A' (Q25, Q26): Gamma, n at x; lambda = -phi'(d) for A members
+__global__ void k_friction_anchor(int n, const int* __restrict__ keys, const double* __restrict__ inA,
+                                  const double* __restrict__ inAp, const double* __restrict__ mu,
+                                  const double* __restrict__ s, double sigma, double dhat,
+                                  const double* __restrict__ x, double* gam, double* nrm, double* lam) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = keys[5 * (size_t)i];
+  const int k = type_nodes(t);
+  d3 P[4];
+  for (int a = 0; a < 4; ++a) P[a] = a < k ? ld3(x, keys[5 * (size_t)i + 1 + a]) : mk(0, 0, 0);
+  const Resolved rs = resolve(t, P[0], P[1], P[2], P[3]);
+  double w[4] = {0, 0, 0, 0};
+  const int* L = rs.loc;
+  if (rs.type == T_PP) {
+    w[L[0]] = 1.0;
+    w[L[1]] = -1.0;
+  } else if (rs.type == T_PE) {
+    const d3 p = P[L[0]], a = P[L[1]], b = P[L[2]];
+    const double tt = dot(p - a, b - a) / dot(b - a, b - a);
+    w[L[0]] = 1.0;
+    w[L[1]] = -(1.0 - tt);
+    w[L[2]] = -tt;
+  } else if (rs.type == T_PT) {
+    const d3 p = P[L[0]], a = P[L[1]], b = P[L[2]], c = P[L[3]];
+    const d3 e1 = b - a, e2 = c - a, ww = p - a;
+    const double a11 = dot(e1, e1), a12 = dot(e1, e2), a22 = dot(e2, e2);
+    const double det = a11 * a22 - a12 * a12;
+    const double u = (a22 * dot(e1, ww) - a12 * dot(e2, ww)) / det;
+    const double v = (a11 * dot(e2, ww) - a12 * dot(e1, ww)) / det;
+    w[L[0]] = 1.0;
+    w[L[1]] = -(1.0 - u - v);
+    w[L[2]] = -u;
+    w[L[3]] = -v;
+  } else {
+    const d3 a0 = P[L[0]], a1 = P[L[1]], b0 = P[L[2]], b1 = P[L[3]];
+    const d3 ea = a1 - a0, eb = b1 - b0, r = a0 - b0;
+    const double A = dot(ea, ea), B = dot(ea, eb), C = dot(eb, eb), D = dot(ea, r), E = dot(eb, r);
+    const double den = A * C - B * B;
+    const double sp = (B * E - C * D) / den, tp = (A * E - B * D) / den;
+    w[L[0]] = 1.0 - sp;
+    w[L[1]] = sp;
+    w[L[2]] = -(1.0 - tp);
+    w[L[3]] = -tp;
+  }
+  d3 diff = mk(0, 0, 0);
+  for (int a = 0; a < k; ++a) diff = diff + w[a] * P[a];
+  const double d = sqrt(dot(diff, diff));
+  for (int a = 0; a < 4; ++a) gam[4 * (size_t)i + a] = w[a];
+  nrm[3 * (size_t)i] = diff.x / d;
+  nrm[3 * (size_t)i + 1] = diff.y / d;
+  nrm[3 * (size_t)i + 2] = diff.z / d;
+  double p1 = 0.0;
+  if (inA[i] != 0.0) p1 += sigma * barrier_b1(d, dhat);
+  if (inAp[i] != 0.0) p1 += -mu[i] + sigma * barrier_b1(d, dhat + s[i]);
+  lam[i] = (inA[i] != 0.0) ? -p1 : 0.0;
+}
+
+__global__ void k_node_contact_grad(int n, const int* __restrict__ rp, const int* __restrict__ col,
+                                    const int* __restrict__ start, const int* __restrict__ codes,
+                                    const double* __restrict__ grad_c, const uint8_t* __restrict__ fixed,
+                                    double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double g[3] = {0, 0, 0};
+  if (!fixed[i] && rp != nullptr) {
+    for (int s = rp[i]; s < rp[i + 1]; ++s) {
+      if (col[s] != i) continue;
+      for (int c = start[s]; c < start[s + 1]; ++c) {
+        const int code = codes[c];
+        const int st = code >> 4, a = (code >> 2) & 3;
+        for (int q = 0; q < 3; ++q) g[q] += grad_c[12 * (size_t)st + 3 * a + q];
+      }
+    }
+  }
+  for (int q = 0; q < 3; ++q) out[3 * (size_t)i + q] = g[q];
+}
+
+__global__ void k_velocity(int n3, const double* __restrict__ x, const double* __restrict__ xt, double inv_h,
+                           double* __restrict__ v) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n3) v[j] = (x[j] - xt[j]) * inv_h;
+}
+__global__ void k_restore_fixed(int n, const double* __restrict__ xt, const uint8_t* __restrict__ fixed, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && fixed[i])
+    for (int c = 0; c < 3; ++c) x[3 * (size_t)i + c] = xt[3 * (size_t)i + c];
+}
+
+struct Energy {
+  double L;
+  int count;
+  double dmin;
+};
+
+double host_scalar(bal_ctx* c, const double* dev) {
+  double v;
+  CK(cudaMemcpyAsync(&v, dev, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return v;
+}
+
+// L(x) at fixed (y, sigma, A' with mu, s, friction anchors) over the swept candidate set (Q37).
+Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand, double sigma) {
+  cudaStream_t st = c->st;
+  const int N = c->N, T = c->T;
+  const double h = c->prm.h, dhat = c->prm.dhat;
+  w.esc.reserve(16);
+  w.evals.reserve(std::max(N, T) + 1);
+  w.cw.part.reserve(kRedBlocks);
+  double* E = w.esc.ptr;
+  // [0] elastic, [1] inertia, [2] barrier, [3] barrier dmin, [4] AL, [5] AL dmin, [6] friction
+  CK(cudaMemsetAsync(E, 0, 8 * sizeof(double), st));
+  if (T > 0) {
+    launch_elastic_energy(st, T, xe, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr, w.evals.ptr);
+    launch_sum(st, T, w.evals.ptr, w.cw.part.ptr, E + 0);
+  }
+  k_inertia_energy<<<ceil_div(N, 256), 256, 0, st>>>(N, xe, c->y.ptr, c->mass.ptr, 0.5 / (h * h), c->fixed.ptr,
+                                                      w.evals.ptr);
+  launch_sum(st, N, w.evals.ptr, w.cw.part.ptr, E + 1);
+  const int n = constraint_set(st, w.cs_trial, cand, xe, dhat);
+  barrier_energy(st, w.cw, w.cs_trial, sigma, dhat, E + 2, E + 3);
+  if (w.n_ap > 0) {
+    w.ap_d.reserve(w.n_ap);
+    key_distances(st, w.n_ap, w.ap_keys.ptr, xe, w.ap_d.ptr);
+    phi_al_energy(st, w.cw, w.n_ap, w.ap_d.ptr, w.ap_mu.ptr, w.ap_s.ptr, sigma, dhat, E + 4, E + 5);
+  } else {
+    const double inf = INFINITY;
+    CK(cudaMemcpyAsync(E + 5, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  if (c->n_fric > 0) {
+    w.evals.reserve(std::max(std::max(N, T), c->n_fric) + 1);
+    launch_friction_energy(st, c->n_fric, xe, c->xt.ptr, c->fr_keys.ptr, c->fr_gam.ptr, c->fr_nrm.ptr, c->fr_lam.ptr,
+                           c->prm.chi, c->prm.eps_v * h, w.evals.ptr);
+    launch_sum(st, c->n_fric, w.evals.ptr, w.cw.part.ptr, E + 6);
+  }
+  double hv[8];
+  CK(cudaMemcpyAsync(hv, E, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  c->launches += 12;
+  Energy r;
+  r.count = n;
+  r.dmin = hv[3];
+  const bool bad = !(hv[3] > 0.0) || !(hv[5] > 0.0) || !std::isfinite(hv[0]);
+  const double L = hv[1] + hv[0] + hv[2] + hv[4] + hv[6];
+  r.L = (bad || !std::isfinite(L)) ? INFINITY : L;
+  return r;
+}
+
+double norm2(bal_ctx* c, const double* v, int n) {
+  launch_dot(c->st, n, v, v, c->red.ptr, c->red.ptr + 1);
+  c->launches += 2;
+  return host_scalar(c, c->red.ptr + 1);
+}
+double dotp(bal_ctx* c, const double* a, const double* b, int n) {
+  launch_dot(c->st, n, a, b, c->red.ptr, c->red.ptr + 2);
+  c->launches += 2;
+  return host_scalar(c, c->red.ptr + 2);
+}
+
+void proximity(bal_ctx* c, StepWork& w, const double* x) {
+  broad_phase(c->st, w.cw, w.cand_prox, c->V, c->sverts.ptr, c->F, c->tris.ptr, c->E, c->edges.ptr, x, x,
+              c->prm.dhat, c->fixed.ptr);
+  constraint_set(c->st, w.cs_A, w.cand_prox, x, c->prm.dhat);
+  c->launches += 16;
+}
+
+double min_d(bal_ctx* c, StepWork& w, const ConstraintSet& cs) {
+  if (cs.n == 0) return INFINITY;
+  w.cw.part.reserve(kRedBlocks);
+  launch_min(c->st, cs.n, cs.d.ptr, w.cw.part.ptr, c->red.ptr + 3);
+  return host_scalar(c, c->red.ptr + 3);
+}
+
+// sigma0 = max(-(g_b . g_E)/||g_b||^2, mean free mass / h^2)  (Q7)
+double sigma0(bal_ctx* c, StepWork& w, const double* x) {
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  const int saved_n = c->cset.n, saved_f = c->n_fric;
+  // g_E = grad (E_I + Psi): assembly with no contact stencils
+  c->cset.n = 0;
+  c->n_fric = 0;
+  run_assembly(c, x, c->y.ptr, 1.0);
+  w.gE.reserve(3 * (size_t)N);
+  CK(cudaMemcpyAsync(w.gE.ptr, c->grad.ptr, 3 * (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  c->cset.n = saved_n;
+  c->n_fric = saved_f;
+  const double floor_ = c->mean_free_mass / (c->prm.h * c->prm.h);
+  if (w.cs_A.n == 0) return floor_;
+  // g_b = sum_A grad b(d; dhat): contact stencils with sigma = 1, inA = 1
+  stencil_union(st, c->ks, w.cs_A.n, w.cs_A.keys.ptr, 0, nullptr, nullptr, nullptr, c->cset);
+  const int ns = c->cset.n;
+  c->stage_c.reserve(90 * (size_t)ns);
+  c->grad_c.reserve(12 * (size_t)ns);
+  c->lbar_c.reserve(ns);
+  c->nodes_c.reserve(4 * (size_t)ns);
+  c->dist_c.reserve(ns);
+  c->dphi_c.reserve(ns);
+  launch_contact(st, ns, x, c->cset.keys.ptr, c->cset.inA.ptr, c->cset.inAp.ptr, c->cset.mu.ptr, c->cset.s.ptr, 1.0,
+                 c->prm.dhat, c->stage_c.ptr, c->grad_c.ptr, c->lbar_c.ptr, c->nodes_c.ptr, c->dist_c.ptr,
+                 c->dphi_c.ptr);
+  build_contact_pattern(st, c->cw, ns, c->nodes_c.ptr, c->fixed.ptr, N, c->stage_c.ptr);
+  w.gb.reserve(3 * (size_t)N);
+  const bool hc = c->cw.nslots > 0;
+  k_node_contact_grad<<<ceil_div(N, 256), 256, 0, st>>>(N, hc ? c->cw.row_ptr.ptr : nullptr,
+                                                         hc ? c->cw.col.ptr : nullptr, hc ? c->cw.start.ptr : nullptr,
+                                                         hc ? c->cw.codes_alt.ptr : nullptr, c->grad_c.ptr,
+                                                         c->fixed.ptr, w.gb.ptr);
+  c->launches += 6;
+  const double bb = norm2(c, w.gb.ptr, 3 * N);
+  if (bb == 0.0) return floor_;
+  const double be = dotp(c, w.gb.ptr, w.gE.ptr, 3 * N);
+  return std::max(-be / bb, floor_);
+}
+
+void rebuild_aprime(bal_ctx* c, StepWork& w) {
+  cudaStream_t st = c->st;
+  const int n = w.cs_A.n;
+  const double thr = 1e-2 * c->prm.dhat;
+  int nn = 0;
+  if (n > 0) {
+    w.sel.reserve(n + 1);
+    w.selcnt.reserve(n + 1);
+    k_flag_lt<<<ceil_div(n, 256), 256, 0, st>>>(n, w.cs_A.d.ptr, thr, w.sel.ptr);
+    size_t t = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t, w.sel.ptr, w.selcnt.ptr, n + 1, st));
+    w.tmp.reserve(t);
+    CK(cudaMemsetAsync(w.sel.ptr + n, 0, sizeof(int), st));
+    CK(cub::DeviceScan::ExclusiveSum(w.tmp.ptr, t, w.sel.ptr, w.selcnt.ptr, n + 1, st));
+    CK(cudaMemcpyAsync(&nn, w.selcnt.ptr + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  w.ap_keys_new.reserve(5 * (size_t)std::max(nn, 1));
+  w.ap_hi_new.reserve(std::max(nn, 1));
+  w.ap_lo_new.reserve(std::max(nn, 1));
+  w.ap_mu_new.reserve(std::max(nn, 1));
+  w.ap_s_new.reserve(std::max(nn, 1));
+  if (nn > 0) {
+    k_compact_keys<<<ceil_div(n, 256), 256, 0, st>>>(n, w.sel.ptr, w.selcnt.ptr, w.cs_A.keys.ptr, w.cs_A.hi.ptr,
+                                                      w.cs_A.lo.ptr, w.ap_keys_new.ptr, w.ap_hi_new.ptr,
+                                                      w.ap_lo_new.ptr);
+    k_carry<<<ceil_div(nn, 256), 256, 0, st>>>(nn, w.ap_hi_new.ptr, w.ap_lo_new.ptr, w.n_ap, w.ap_hi.ptr, w.ap_lo.ptr,
+                                               w.ap_mu.ptr, w.ap_s.ptr, w.ap_mu_new.ptr, w.ap_s_new.ptr);
+    CK(cudaGetLastError());
+  }
+  std::swap(w.ap_keys.ptr, w.ap_keys_new.ptr);
+  std::swap(w.ap_keys.cap, w.ap_keys_new.cap);
+  std::swap(w.ap_hi.ptr, w.ap_hi_new.ptr);
+  std::swap(w.ap_hi.cap, w.ap_hi_new.cap);
+  std::swap(w.ap_lo.ptr, w.ap_lo_new.ptr);
+  std::swap(w.ap_lo.cap, w.ap_lo_new.cap);
+  std::swap(w.ap_mu.ptr, w.ap_mu_new.ptr);
+  std::swap(w.ap_mu.cap, w.ap_mu_new.cap);
+  std::swap(w.ap_s.ptr, w.ap_s_new.ptr);
+  std::swap(w.ap_s.cap, w.ap_s_new.cap);
+  w.n_ap = nn;
+  c->launches += 4;
+}
+
+struct StepFail : std::runtime_error {
+  bal_status st;
+  StepFail(bal_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_next, double* v_next,
+                   bal_step_stats* stats) {
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  if (!c->sw) c->sw = new StepWork();
+  StepWork& w = *c->sw;
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  const size_t n3 = 3 * (size_t)N;
+  const bal_params& P = c->prm;
+  const double h = P.h, dhat = P.dhat;
+  bal_step_stats S;
+  std::memset(&S, 0, sizeof(S));
+  c->trace.clear();
+  for (auto* b : {&w.x, &w.xn, &w.dir, &w.rhs, &w.trial, &w.v}) b->reserve(n3);
+  CK(cudaMemcpyAsync(c->xt.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  k_predictor<<<ceil_div(N, 256), 256, 0, st>>>(N, x_t, v_t, h, P.gravity[0], P.gravity[1], P.gravity[2],
+                                                 c->fixed.ptr, c->y.ptr);
+  CK(cudaMemcpyAsync(w.x.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  w.n_ap = 0;
+  c->n_fric = 0;
+  auto t0 = clk::now();
+  proximity(c, w, w.x.ptr);
+  double dmin = min_d(c, w, w.cs_A);
+  S.ms_collision += ms_since(t0);
+  if (!(dmin > 0.0)) throw StepFail(BAL_E_INFEASIBLE, "bal_step: input has a surface distance <= 0");
+  t0 = clk::now();
+  const double sig0 = sigma0(c, w, w.x.ptr);
+  S.ms_assembly += ms_since(t0);
+  double sigma = sig0;
+  double dmin_prev = INFINITY;
+  double e0 = -1.0;
+  bool converged = false;
+  const bool no_al = (P.flags & BAL_NO_AUGLAG) != 0;
+  for (int l = 0; l < P.max_newton; ++l) {
+    if (l > 0) {
+      t0 = clk::now();
+      proximity(c, w, w.x.ptr);
+      dmin = min_d(c, w, w.cs_A);
+      S.ms_collision += ms_since(t0);
+    }
+    S.max_constraints = std::max(S.max_constraints, w.cs_A.n);
+    // A' rules (Alg. 1 lines 3-6)
+    int rebuilt = 0;
+    if (!no_al) {
+      if (dmin > 1e-2 * dhat) {
+        w.n_ap = 0;
+      } else if (dmin < dmin_prev || w.n_ap == 0) {
+        rebuild_aprime(c, w);
+        rebuilt = 1;
+      }
+    }
+    dmin_prev = dmin;
+    S.max_aprime = std::max(S.max_aprime, w.n_ap);
+    // contact stencils = A u A' (Q22)
+    t0 = clk::now();
+    stencil_union(st, c->ks, w.cs_A.n, w.cs_A.keys.ptr, w.n_ap, w.ap_keys.ptr, w.ap_mu.ptr, w.ap_s.ptr, c->cset);
+    // friction anchors at x^l
+    c->n_fric = 0;
+    if (P.chi > 0.0 && c->cset.n > 0) {
+      const int nc = c->cset.n;
+      c->fr_keys.reserve(5 * (size_t)nc);
+      c->fr_gam.reserve(4 * (size_t)nc);
+      c->fr_nrm.reserve(3 * (size_t)nc);
+      c->fr_lam.reserve(nc);
+      CK(cudaMemcpyAsync(c->fr_keys.ptr, c->cset.keys.ptr, 5 * (size_t)nc * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      k_friction_anchor<<<ceil_div(nc, 128), 128, 0, st>>>(nc, c->cset.keys.ptr, c->cset.inA.ptr, c->cset.inAp.ptr,
+                                                           c->cset.mu.ptr, c->cset.s.ptr, sigma, dhat, w.x.ptr,
+                                                           c->fr_gam.ptr, c->fr_nrm.ptr, c->fr_lam.ptr);
+      c->n_fric = nc;
+    }
+    run_assembly(c, w.x.ptr, c->y.ptr, sigma);
+    const double en = std::sqrt(norm2(c, c->grad.ptr, 3 * N));
+    S.ms_assembly += ms_since(t0);
+    if (e0 < 0) e0 = en;
+    if (e0 == 0.0) {
+      converged = true;
+      break;
+    }
+    // Newton direction: A p = -e with warm start + PCG (App. B)
+    launch_axpy(st, 3 * N, -2.0, c->grad.ptr, c->grad.ptr, w.rhs.ptr);  // rhs = e - 2e = -e
+    t0 = clk::now();
+    bal_pcg_stats ps;
+    const bool warm = !(P.flags & BAL_NO_WARMSTART);
+    pcg_solve(c, w.rhs.ptr, nullptr, w.dir.ptr, warm, P.pcg_rel_tol, P.pcg_stall_window, P.max_pcg, P.ws_rel_tol,
+              P.ws_max_iters, &ps);
+    CK(cudaStreamSynchronize(st));
+    S.ms_pcg += ms_since(t0);
+    S.ws_iters += ps.ws_iters_max;
+    int resumes = 0, halvings = 0, safeguard = 0;
+    double alpha = 0.0, a_ccd = 1.0;
+    t0 = clk::now();
+    while (true) {
+      if (dotp(c, w.dir.ptr, c->grad.ptr, 3 * N) >= 0.0) {  // Q38 descent safeguard
+        launch_apply_dinv(st, N, c->dinv.ptr, c->grad.ptr, w.dir.ptr, -1.0);
+        safeguard = 1;
+      }
+      // swept candidates x -> x + p, CCD
+      launch_axpy(st, 3 * N, 1.0, w.dir.ptr, w.x.ptr, w.trial.ptr);
+      broad_phase(st, w.cw, w.cand_sw, c->V, c->sverts.ptr, c->F, c->tris.ptr, c->E, c->edges.ptr, w.x.ptr,
+                  w.trial.ptr, dhat, c->fixed.ptr);
+      a_ccd = ccd_step_toi(st, w.cw, w.cand_sw, w.x.ptr, w.dir.ptr, dhat);
+      alpha = std::min(1.0, a_ccd);
+      const Energy E0 = energy(c, w, w.x.ptr, w.cand_sw, sigma);
+      halvings = 0;
+      bool ok = false;
+      while (alpha >= P.alpha_min) {
+        launch_axpy(st, 3 * N, alpha, w.dir.ptr, w.x.ptr, w.trial.ptr);
+        const Energy E1 = energy(c, w, w.trial.ptr, w.cand_sw, sigma);
+        if (E1.count <= P.max_constraints && E1.L <= E0.L) {
+          ok = true;
+          break;
+        }
+        alpha *= 0.5;
+        ++halvings;
+      }
+      if (ok) break;
+      if (resumes >= 50 || c->h_scal->k >= P.max_pcg) {
+        S.ms_linesearch += ms_since(t0);
+        throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: line search failed after PCG resumes");
+      }
+      ++resumes;
+      pcg_resume(c, P.pcg_resume_iters, w.dir.ptr, &ps);
+    }
+    S.ms_linesearch += ms_since(t0);
+    S.newton_iters += 1;
+    S.pcg_iters += c->h_scal->k;
+    S.last_rel_grad = en / e0;
+    const double rec[BAL_TRACE_FIELDS] = {(double)l, (double)w.cs_A.n, (double)w.n_ap, (double)rebuilt, dmin, sigma,
+                                          (double)ps.ws_iters_max, (double)c->h_scal->k, (double)c->h_scal->stop,
+                                          a_ccd, alpha, (double)halvings, (double)resumes, (double)safeguard,
+                                          en / e0};
+    c->trace.insert(c->trace.end(), rec, rec + BAL_TRACE_FIELDS);
+    // x^{l+1} is in w.trial; its constraint set is w.cs_trial
+    if (en <= P.newton_rel_tol * e0) {
+      std::swap(w.x.ptr, w.trial.ptr);
+      converged = true;
+      break;
+    }
+    if (w.n_ap > 0) {  // Alg. 1 lines 12-14
+      w.ap_d.reserve(w.n_ap);
+      key_distances(st, w.n_ap, w.ap_keys.ptr, w.trial.ptr, w.ap_d.ptr);
+      k_al_update<<<ceil_div(w.n_ap, 256), 256, 0, st>>>(w.n_ap, w.ap_d.ptr, sigma, dhat, w.ap_mu.ptr, w.ap_s.ptr);
+      c->launches += 2;
+    }
+    if (!no_al) {  // Alg. 1 lines 15-16
+      const double dnew = min_d(c, w, w.cs_trial);
+      if (dnew < 1e-2 * dhat) sigma = std::max(1.2 * sigma, 100.0 * sig0);
+    }
+    std::swap(w.x.ptr, w.trial.ptr);
+  }
+  k_restore_fixed<<<ceil_div(N, 256), 256, 0, st>>>(N, c->xt.ptr, c->fixed.ptr, w.x.ptr);
+  CK(cudaMemcpyAsync(x_next, w.x.ptr, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (v_next) k_velocity<<<ceil_div((int)n3, 256), 256, 0, st>>>((int)n3, w.x.ptr, c->xt.ptr, 1.0 / h, v_next);
+  CK(cudaStreamSynchronize(st));
+  S.sigma0 = sig0;
+  S.sigma_final = sigma;
+  S.min_distance = dmin;
+  S.ms_total = ms_since(t_start);
+  if (stats) *stats = S;
+  if (!converged) throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: Newton iteration cap reached");
+  return BAL_OK;
+}
+
+template <typename F>
+bal_status guard_step(bal_ctx* c, F&& f) {
+  try {
+    CK(cudaSetDevice(c->device));
+    return f();
+  } catch (const StepFail& e) {
+    c->err = e.what();
+    return e.st;
+  } catch (const OomError& e) {
+    c->err = e.what();
+    return BAL_E_OOM;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return BAL_E_CUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+bal_status bal_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_next, double* v_next,
+                    bal_step_stats* stats) {
+  if (!c || !x_t || !v_t || !x_next) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() { return do_step(c, x_t, v_t, x_next, v_next, stats); });
+}
+
+bal_status bal_step_host(bal_ctx* c, const double* x_t, const double* v_t, double* x_next, double* v_next,
+                         bal_step_stats* stats) {
+  if (!c || !x_t || !v_t || !x_next) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() {
+    const size_t n3 = 3 * (size_t)c->N;
+    DevBuf<double> dx, dv, dxn, dvn;
+    dx.upload(x_t, n3, c->st);
+    dv.upload(v_t, n3, c->st);
+    dxn.reserve(n3);
+    dvn.reserve(n3);
+    const bal_status s = do_step(c, dx.ptr, dv.ptr, dxn.ptr, dvn.ptr, stats);
+    CK(cudaMemcpyAsync(x_next, dxn.ptr, n3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (v_next) CK(cudaMemcpyAsync(v_next, dvn.ptr, n3 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return s;
+  });
+}
+
+int32_t bal_get_trace(const bal_ctx* c, double* out, int32_t max_records) {
+  if (!c || !out || max_records < 0) return BAL_E_INVALID_ARG;
+  const int n = (int)(c->trace.size() / BAL_TRACE_FIELDS);
+  const int m = std::min(n, max_records);
+  std::memcpy(out, c->trace.data(), sizeof(double) * m * BAL_TRACE_FIELDS);
+  return m;
+}
+
+}  // extern "C"

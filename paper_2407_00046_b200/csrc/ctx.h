@@ -1,0 +1,80 @@
+// ctx.h -- the opaque bal_ctx: device-resident mesh, static pattern, per-iteration buffers.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/bal.h"
+#include "assemble.h"
+#include "kernels.h"
+#include "keys.h"
+
+struct bal_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t st = nullptr;
+  bal_params prm{};
+  int N = 0, T = 0;
+  std::string err;
+  long long launches = 0;
+
+  // ---- mesh (device)
+  bal::DevBuf<int4> tets;
+  bal::DevBuf<double> Dm_inv, vol, mu, lam, mass;
+  bal::DevBuf<uint8_t> fixed;
+  std::vector<uint8_t> h_fixed;
+  std::vector<double> h_mass;
+  double mean_free_mass = 0.0;
+  int n_free = 0;
+  // surface
+  int F = 0, E = 0, V = 0;
+  bal::DevBuf<int> tris, edges, sverts;
+  // ---- static pattern (device)
+  bal::DevBuf<int> sp_row_ptr, sp_col, sp_slot_row, sp_diag_pos, sp_slot_ptr, sp_slot_code;
+  bal::StaticPattern sp;
+  bal::DevBuf<double> sval;
+  // ---- elastic stencils
+  bal::DevBuf<double> stage_e, grad_e, lbar_e;
+  // ---- contact + friction stencils (friction appended after contact)
+  bal::StencilSet cset;
+  int n_contact = 0, n_fric = 0;
+  bal::DevBuf<double> stage_c, grad_c, lbar_c, dist_c, dphi_c;
+  bal::DevBuf<int> nodes_c;
+  bal::DevBuf<int> fr_keys;
+  bal::DevBuf<double> fr_gam, fr_nrm, fr_lam;
+  bal::ContactWork cw;
+  bal::KeySorter ks;
+  // ---- system
+  bal::DevBuf<double> grad, e_node, dinv, y, xt;
+  bal::DevBuf<int> group, grp_c;
+  bool loaded_bsr = false;  // test path: system injected by bal_load_bsr
+  bal::DevBuf<int> lb_row_ptr, lb_col;
+  bal::DevBuf<double> lb_val;
+  int lb_nnzb = 0;
+  // ---- PCG
+  bal::DevBuf<double> pr, pz, pp, pq, px, partials, hist;
+  bal::DevBuf<unsigned> counter;
+  bal::DevBuf<bal::PcgScal> scal;
+  bal::DevBuf<bal::GrpScal> gscal;
+  bal::PcgScal* h_scal = nullptr;  // pinned
+  int ngroups = 0;
+  // scratch
+  bal::DevBuf<double> tmp_a, tmp_b, red;
+  bal::DevBuf<int> tmp_i;
+
+  // ---- time-step work (bal_step.cu), allocated on first use
+  struct StepWork* sw = nullptr;
+  std::vector<double> trace;  // per-Newton-iteration decision trace of the last bal_step
+
+  bal::Bsr static_bsr() const;
+  bal::Bsr contact_bsr() const;
+};
+
+void destroy_step_work(bal_ctx* c);
+
+namespace bal {
+void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma);
+void compact_groups(bal_ctx* c);
+int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
+              int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats);
+void pcg_resume(bal_ctx* c, int extra, double* x_out, bal_pcg_stats* stats);
+}  // namespace bal

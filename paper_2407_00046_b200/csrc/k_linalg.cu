@@ -1,0 +1,590 @@
+// k_linalg.cu -- BSR3 SpMV, block-Jacobi PCG and the stiffness-grouped warm start
+// (SURVEY §8(a) a7, a8, a9).
+//
+// SpMV: y = A v with A stored as a static full BSR over the mesh adjacency plus a
+// per-Newton-iteration contact/friction BSR (the paper's D+L+L^T and sum C_i + C_i^T, kept as
+// two row-owned parts so no atomics are needed).  Sub-warp of kSL lanes per block row: the row's
+// 9*nnz doubles are contiguous, so lanes stream them perfectly coalesced; each lane accumulates
+// into the 3 row components and the sub-warp reduces with shuffles.
+// PCG (App. B): textbook preconditioned CG (same recurrences as the
+// oracle) with M = blockdiag(D_j)^{-1} stored symmetric (6 doubles / node).  Reductions are
+// deterministic: fixed grid, per-block partials, the last block (atomic ticket) reduces them in
+// a fixed order and computes alpha / beta / stop flags on the device -- no host round trip.
+// Warm start (Q20): per-group PCG on A_GG, masked SpMV (cross-group blocks
+// skipped), per-group scalars in one GrpScal, group-wise deterministic warp-match reductions.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace bal {
+
+constexpr int kSL = 16;        // lanes per block row
+constexpr int kSpmvThreads = 256;
+constexpr int kSpmvBlocks = 16 * kSMs;
+
+template <bool MASK>
+BAL_D void row_accum(const Bsr& A, int row, int lane, const double* __restrict__ v, const int* __restrict__ grp,
+                     int gr, double& a0, double& a1, double& a2) {
+  const int beg = __ldg(A.row_ptr + row), end = __ldg(A.row_ptr + row + 1);
+  const double* __restrict__ vals = A.val + 9 * (size_t)beg;
+  const int nf = 9 * (end - beg);
+  int f = lane;
+  int blk = f / 9;
+  int rem = f - 9 * blk;
+  for (; f < nf; f += kSL) {
+    const int col = __ldg(A.col + beg + blk);
+    const double a = __ldcs(vals + f);  // streamed once per SpMV: evict-first
+    const int r = rem / 3, c = rem - 3 * r;
+    double pr = a * __ldg(v + 3 * (size_t)col + c);
+    if (MASK && __ldg(grp + col) != gr) pr = 0.0;
+    if (r == 0) a0 += pr;
+    else if (r == 1) a1 += pr;
+    else a2 += pr;
+    rem += kSL % 9;
+    blk += kSL / 9;
+    if (rem >= 9) {
+      rem -= 9;
+      ++blk;
+    }
+  }
+}
+
+template <bool DOT, bool MASK>
+__global__ void __launch_bounds__(kSpmvThreads)
+k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, double* __restrict__ y,
+       double* partials, unsigned* counter, PcgScal* sc, const GrpScal* gs) {
+  if (DOT && sc->done) return;
+  const int n = S.n;
+  const int lane = threadIdx.x & (kSL - 1);
+  const int sub_in_warp = (threadIdx.x & 31) / kSL;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  constexpr int kRowsPerWarp = 32 / kSL;
+  double dacc = 0.0;
+  for (int base = gwarp * kRowsPerWarp; base < n; base += nwarps * kRowsPerWarp) {
+    const int row = base + sub_in_warp;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    bool valid = row < n;
+    int gr = 0;
+    if (MASK && valid) {
+      gr = grp[row];
+      valid = gr >= 0 && gs->active[gr];
+    }
+    if (valid) {
+      row_accum<MASK>(S, row, lane, v, grp, gr, a0, a1, a2);
+      if (C.nnzb > 0) row_accum<MASK>(C, row, lane, v, grp, gr, a0, a1, a2);
+    }
+#pragma unroll
+    for (int o = kSL / 2; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (valid && lane == 0) {
+      y[3 * (size_t)row] = a0;
+      y[3 * (size_t)row + 1] = a1;
+      y[3 * (size_t)row + 2] = a2;
+      if (DOT) dacc += v[3 * (size_t)row] * a0 + v[3 * (size_t)row + 1] * a1 + v[3 * (size_t)row + 2] * a2;
+    }
+  }
+  if (DOT) {
+    __shared__ double sh[kSpmvThreads / 32];
+    __shared__ bool last;
+    const double bs = block_sum<kSpmvThreads>(dacc, sh);
+    if (threadIdx.x == 0) {
+      partials[blockIdx.x] = bs;
+      __threadfence();
+      last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      double t = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += partials[i];
+      t = block_sum<kSpmvThreads>(t, sh);
+      if (threadIdx.x == 0) {
+        sc->pq = t;
+        sc->alpha = sc->rz / t;
+        *counter = 0u;
+      }
+    }
+  }
+}
+
+void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y) {
+  if (S.n <= 0) return;
+  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  k_spmv<false, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, nullptr, nullptr, nullptr, nullptr);
+  CK(cudaGetLastError());
+}
+
+void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* partials,
+                     unsigned* counter, PcgScal* sc) {
+  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  k_spmv<true, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, partials, counter, sc, nullptr);
+  CK(cudaGetLastError());
+}
+
+void launch_spmv_masked(cudaStream_t st, const Bsr& S, const Bsr& C, const int* grp, const double* v, double* y,
+                        const GrpScal* gs) {
+  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  k_spmv<false, true><<<blocks, kSpmvThreads, 0, st>>>(S, C, grp, v, y, nullptr, nullptr, nullptr, gs);
+  CK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------- vectors
+BAL_D void dinv_apply(const double* __restrict__ dinv, int i, double r0, double r1, double r2, double& z0,
+                      double& z1, double& z2) {
+  const double* m = dinv + 6 * (size_t)i;
+  z0 = m[0] * r0 + m[1] * r1 + m[2] * r2;
+  z1 = m[1] * r0 + m[3] * r1 + m[4] * r2;
+  z2 = m[2] * r0 + m[4] * r1 + m[5] * r2;
+}
+
+// last-block finalisation helper for NQ quantities
+template <int NQ, int NT>
+BAL_D bool last_block_reduce(const double (&loc)[NQ], double* partials, unsigned* counter, double (&tot)[NQ]) {
+  __shared__ double sh[NT / 32];
+  __shared__ bool last;
+  double bs[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) bs[q] = block_sum<NT>(loc[q], sh);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) partials[NQ * blockIdx.x + q] = bs[q];
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += partials[NQ * i + q];
+    tot[q] = block_sum<NT>(t, sh);
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+// App. B stop logic (oracle.linalg.pcg_run order): NaN, converged, stagnation, cap.
+BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
+  const int k = sc->k;
+  const double rn = hist[k];
+  if (!isfinite(rn)) {
+    sc->stop = 3;
+    sc->done = 1;
+    return;
+  }
+  if (rn <= sc->tol * sc->bnorm) {
+    sc->stop = 0;
+    sc->done = 1;
+    return;
+  }
+  const int W = sc->window;
+  if (W > 0 && k >= W) {
+    double older = sc->min_old;  // min over hist[0 .. k-W]
+    double recent = hist[k];
+    for (int j = k - W + 1; j < k; ++j) recent = fmin(recent, hist[j]);
+    if (recent >= older) {
+      sc->stop = 1;
+      sc->done = 1;
+      return;
+    }
+  }
+  if (k >= sc->max_iters) {
+    sc->stop = 2;
+    sc->done = 1;
+  }
+}
+
+constexpr int kVecThreads = 256;
+constexpr int kVecBlocks = 4 * kSMs;
+
+__global__ void __launch_bounds__(kVecThreads)
+k_pcg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, const double* __restrict__ dinv,
+           double* __restrict__ r, double* __restrict__ z, double* __restrict__ p, double* partials,
+           unsigned* counter, PcgScal* sc, double* hist) {
+  double loc[3] = {0.0, 0.0, 0.0};  // rz, rr, bb
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double rr[3], bb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      bb[c] = b[3 * (size_t)i + c];
+      rr[c] = bb[c] - Ax0[3 * (size_t)i + c];
+      r[3 * (size_t)i + c] = rr[c];
+    }
+    double z0, z1, z2;
+    dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
+    z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
+    p[3 * (size_t)i] = z0; p[3 * (size_t)i + 1] = z1; p[3 * (size_t)i + 2] = z2;
+    loc[0] += rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
+    loc[1] += rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+    loc[2] += bb[0] * bb[0] + bb[1] * bb[1] + bb[2] * bb[2];
+  }
+  double tot[3];
+  if (last_block_reduce<3, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
+    sc->rz = tot[0];
+    sc->rr = tot[1];
+    sc->bnorm = sqrt(tot[2]);
+    sc->k = 0;
+    sc->stop = -1;
+    sc->done = 0;
+    sc->min_old = INFINITY;
+    hist[0] = sqrt(tot[1]);
+    pcg_stop_check(sc, hist);
+  }
+}
+
+void launch_pcg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
+                     double* z, double* p, double* partials, unsigned* counter, PcgScal* sc, double* hist) {
+  k_pcg_init<<<kVecBlocks, kVecThreads, 0, st>>>(n, b, Ax0, dinv, r, z, p, partials, counter, sc, hist);
+  CK(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+k_pcg_update(int n, const double* __restrict__ dinv, const double* __restrict__ p, const double* __restrict__ q,
+             double* __restrict__ x, double* __restrict__ r, double* __restrict__ z, double* partials,
+             unsigned* counter, PcgScal* sc, double* hist) {
+  if (sc->done) return;
+  const double alpha = sc->alpha;
+  double loc[2] = {0.0, 0.0};  // rz, rr
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double rr[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const size_t j = 3 * (size_t)i + c;
+      x[j] = x[j] + alpha * p[j];
+      rr[c] = r[j] - alpha * q[j];
+      r[j] = rr[c];
+    }
+    double z0, z1, z2;
+    dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
+    z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
+    loc[0] += rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
+    loc[1] += rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+  }
+  double tot[2];
+  if (last_block_reduce<2, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
+    sc->beta = tot[0] / sc->rz;
+    sc->rz = tot[0];
+    sc->rr = tot[1];
+    const int k = sc->k + 1;
+    sc->k = k;
+    hist[k] = sqrt(tot[1]);
+    if (sc->window > 0 && k - sc->window >= 0) sc->min_old = fmin(sc->min_old, hist[k - sc->window]);
+    pcg_stop_check(sc, hist);
+  }
+}
+
+void launch_pcg_update(cudaStream_t st, int n, const double* dinv, const double* p, const double* q, double* x,
+                       double* r, double* z, double* partials, unsigned* counter, PcgScal* sc, double* hist) {
+  k_pcg_update<<<kVecBlocks, kVecThreads, 0, st>>>(n, dinv, p, q, x, r, z, partials, counter, sc, hist);
+  CK(cudaGetLastError());
+}
+
+__global__ void k_pcg_pupdate(int n3, const double* __restrict__ z, double* __restrict__ p, const PcgScal* sc) {
+  if (sc->done) return;
+  const double beta = sc->beta;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n3; j += gridDim.x * blockDim.x) p[j] = z[j] + beta * p[j];
+}
+
+void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc) {
+  k_pcg_pupdate<<<kVecBlocks, kVecThreads, 0, st>>>(3 * n, z, p, sc);
+  CK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------- grouped (warm start)
+template <int NQ>
+BAL_D void grp_warp_accum(int g, const double (&v)[NQ], double* bucket /*[warps][kMaxGroups][NQ]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned pending = __ballot_sync(0xffffffffu, g >= 0);
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const int gl = __shfl_sync(0xffffffffu, g, leader);
+    const unsigned members = __ballot_sync(0xffffffffu, g == gl);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double s = (g == gl) ? v[q] : 0.0;
+      s = warp_sum(s);
+      if (lane == leader) bucket[(w * kMaxGroups + gl) * NQ + q] += s;
+    }
+    pending &= ~members;
+  }
+}
+
+// block buckets -> per-block partials [blk][kMaxGroups][NQ]; last block -> totals (thread g)
+template <int NQ>
+BAL_D bool grp_finish(double* bucket, double* partials, unsigned* counter, int G, double (&tot)[NQ]) {
+  __shared__ bool last;
+  constexpr int W = kVecThreads / 32;
+  __syncthreads();
+  for (int t = threadIdx.x; t < G * NQ; t += blockDim.x) {
+    const int g = t / NQ, q = t % NQ;
+    double s = 0.0;
+    for (int w = 0; w < W; ++w) s += bucket[(w * kMaxGroups + g) * NQ + q];
+    partials[((size_t)blockIdx.x * kMaxGroups + g) * NQ + q] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  if (threadIdx.x < G) {
+    const int g = threadIdx.x;
+    for (int q = 0; q < NQ; ++q) {
+      double s = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) s += partials[((size_t)b * kMaxGroups + g) * NQ + q];
+      tot[q] = s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+BAL_D void ws_zero_bucket(double* bucket, int nq) {
+  for (int t = threadIdx.x; t < (kVecThreads / 32) * kMaxGroups * nq; t += blockDim.x) bucket[t] = 0.0;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+k_ws_init(int n, const int* __restrict__ grp, const double* __restrict__ b, const double* __restrict__ dinv,
+          double* __restrict__ x, double* __restrict__ r, double* __restrict__ z, double* __restrict__ p,
+          double* partials, unsigned* counter, GrpScal* gs) {
+  __shared__ double bucket[(kVecThreads / 32) * kMaxGroups * 2];
+  ws_zero_bucket(bucket, 2);
+  const int G = gs->ngroups;
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int i = base + threadIdx.x;
+    int g = -1;
+    double v[2] = {0.0, 0.0};  // rz, rr
+    if (i < n) {
+      g = grp[i];
+      double rr[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        rr[c] = (g >= 0) ? b[3 * (size_t)i + c] : 0.0;
+        r[3 * (size_t)i + c] = rr[c];
+        x[3 * (size_t)i + c] = 0.0;
+      }
+      double z0, z1, z2;
+      dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
+      z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
+      p[3 * (size_t)i] = z0; p[3 * (size_t)i + 1] = z1; p[3 * (size_t)i + 2] = z2;
+      v[0] = rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
+      v[1] = rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+    }
+    grp_warp_accum<2>(g, v, bucket);
+  }
+  double tot[2];
+  if (grp_finish<2>(bucket, partials, counter, G, tot)) {
+    if (threadIdx.x < G) {
+      const int g = threadIdx.x;
+      gs->rz[g] = tot[0];
+      gs->rr[g] = tot[1];
+      gs->bnorm[g] = sqrt(tot[1]);
+      gs->iters[g] = 0;
+      const double rn = sqrt(tot[1]);
+      gs->active[g] = (isfinite(rn) && !(rn <= gs->tol * gs->bnorm[g]) && gs->max_iters > 0) ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int g = 0; g < G; ++g) any |= gs->active[g];
+      gs->any_active = any;
+    }
+  }
+}
+
+void launch_ws_init(cudaStream_t st, int n, const int* grp, const double* b, const double* dinv, double* x,
+                    double* r, double* z, double* p, double* partials, unsigned* counter, GrpScal* gs) {
+  k_ws_init<<<kVecBlocks, kVecThreads, 0, st>>>(n, grp, b, dinv, x, r, z, p, partials, counter, gs);
+  CK(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+k_ws_dot(int n, const int* __restrict__ grp, const double* __restrict__ p, const double* __restrict__ q,
+         double* partials, unsigned* counter, GrpScal* gs) {
+  if (!gs->any_active) return;
+  __shared__ double bucket[(kVecThreads / 32) * kMaxGroups * 1];
+  ws_zero_bucket(bucket, 1);
+  const int G = gs->ngroups;
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int i = base + threadIdx.x;
+    int g = -1;
+    double v[1] = {0.0};
+    if (i < n) {
+      g = grp[i];
+      if (g >= 0 && gs->active[g]) {
+        const size_t j = 3 * (size_t)i;
+        v[0] = p[j] * q[j] + p[j + 1] * q[j + 1] + p[j + 2] * q[j + 2];
+      } else {
+        g = -1;
+      }
+    }
+    grp_warp_accum<1>(g, v, bucket);
+  }
+  double tot[1];
+  if (grp_finish<1>(bucket, partials, counter, G, tot)) {
+    if (threadIdx.x < G && gs->active[threadIdx.x]) {
+      gs->pq[threadIdx.x] = tot[0];
+      gs->alpha[threadIdx.x] = gs->rz[threadIdx.x] / tot[0];
+    }
+  }
+}
+
+void launch_ws_dot(cudaStream_t st, int n, const int* grp, const double* p, const double* q, double* partials,
+                   unsigned* counter, GrpScal* gs) {
+  k_ws_dot<<<kVecBlocks, kVecThreads, 0, st>>>(n, grp, p, q, partials, counter, gs);
+  CK(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+k_ws_update(int n, const int* __restrict__ grp, const double* __restrict__ dinv, const double* __restrict__ p,
+            const double* __restrict__ q, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+            double* partials, unsigned* counter, GrpScal* gs) {
+  if (!gs->any_active) return;
+  __shared__ double bucket[(kVecThreads / 32) * kMaxGroups * 2];
+  ws_zero_bucket(bucket, 2);
+  const int G = gs->ngroups;
+  const int stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int i = base + threadIdx.x;
+    int g = -1;
+    double v[2] = {0.0, 0.0};
+    if (i < n) {
+      g = grp[i];
+      if (g >= 0 && gs->active[g]) {
+        const double alpha = gs->alpha[g];
+        double rr[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const size_t j = 3 * (size_t)i + c;
+          x[j] = x[j] + alpha * p[j];
+          rr[c] = r[j] - alpha * q[j];
+          r[j] = rr[c];
+        }
+        double z0, z1, z2;
+        dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
+        z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
+        v[0] = rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
+        v[1] = rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+      } else {
+        g = -1;
+      }
+    }
+    grp_warp_accum<2>(g, v, bucket);
+  }
+  double tot[2];
+  if (grp_finish<2>(bucket, partials, counter, G, tot)) {
+    if (threadIdx.x < G && gs->active[threadIdx.x]) {
+      const int g = threadIdx.x;
+      gs->beta[g] = tot[0] / gs->rz[g];
+      gs->rz[g] = tot[0];
+      gs->rr[g] = tot[1];
+      gs->iters[g] += 1;
+      const double rn = sqrt(tot[1]);
+      const bool stop = !isfinite(rn) || rn <= gs->tol * gs->bnorm[g] || gs->iters[g] >= gs->max_iters;
+      if (stop) gs->active[g] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int g = 0; g < G; ++g) any |= gs->active[g];
+      gs->any_active = any;
+    }
+  }
+}
+
+void launch_ws_update(cudaStream_t st, int n, const int* grp, const double* dinv, const double* p, const double* q,
+                      double* x, double* r, double* z, double* partials, unsigned* counter, GrpScal* gs) {
+  k_ws_update<<<kVecBlocks, kVecThreads, 0, st>>>(n, grp, dinv, p, q, x, r, z, partials, counter, gs);
+  CK(cudaGetLastError());
+}
+
+__global__ void k_ws_pupdate(int n, const int* __restrict__ grp, const double* __restrict__ z, double* __restrict__ p,
+                             const GrpScal* gs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int g = grp[i];
+    if (g >= 0 && gs->active[g]) {
+      const double beta = gs->beta[g];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) p[3 * (size_t)i + c] = z[3 * (size_t)i + c] + beta * p[3 * (size_t)i + c];
+    }
+  }
+}
+
+void launch_ws_pupdate(cudaStream_t st, int n, const int* grp, const double* z, double* p, const GrpScal* gs) {
+  k_ws_pupdate<<<kVecBlocks, kVecThreads, 0, st>>>(n, grp, z, p, gs);
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------- generic reductions
+__global__ void k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b, double* partials) {
+  __shared__ double sh[kRedThreads / 32];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    s += a[i] * (b ? b[i] : 1.0);
+  s = block_sum<kRedThreads>(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void k_min_part(int n, const double* __restrict__ a, double* partials) {
+  __shared__ double sh[kRedThreads / 32];
+  double s = INFINITY;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) s = fmin(s, a[i]);
+  s = block_min<kRedThreads>(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void k_finish(int np, const double* partials, double* out, int is_min) {
+  __shared__ double sh[kRedThreads / 32];
+  double s = is_min ? INFINITY : 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s = is_min ? fmin(s, partials[i]) : s + partials[i];
+  s = is_min ? block_min<kRedThreads>(s, sh) : block_sum<kRedThreads>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+void launch_dot(cudaStream_t st, int n, const double* a, const double* b, double* partials, double* out) {
+  k_dot_part<<<kRedBlocks, kRedThreads, 0, st>>>(n, a, b, partials);
+  k_finish<<<1, kRedThreads, 0, st>>>(kRedBlocks, partials, out, 0);
+  CK(cudaGetLastError());
+}
+void launch_sum(cudaStream_t st, int n, const double* a, double* partials, double* out) {
+  launch_dot(st, n, a, nullptr, partials, out);
+}
+void launch_min(cudaStream_t st, int n, const double* a, double* partials, double* out) {
+  k_min_part<<<kRedBlocks, kRedThreads, 0, st>>>(n, a, partials);
+  k_finish<<<1, kRedThreads, 0, st>>>(kRedBlocks, partials, out, 1);
+  CK(cudaGetLastError());
+}
+
+__global__ void k_axpy(int n, double alpha, const double* __restrict__ x, const double* __restrict__ y,
+                       double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = y[i] + alpha * x[i];
+}
+void launch_axpy(cudaStream_t st, int n, double alpha, const double* x, const double* y, double* out) {
+  k_axpy<<<kVecBlocks, kVecThreads, 0, st>>>(n, alpha, x, y, out);
+  CK(cudaGetLastError());
+}
+
+__global__ void k_apply_dinv(int nn, const double* __restrict__ dinv, const double* __restrict__ r,
+                             double* __restrict__ z, double scale) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+    double z0, z1, z2;
+    dinv_apply(dinv, i, r[3 * (size_t)i], r[3 * (size_t)i + 1], r[3 * (size_t)i + 2], z0, z1, z2);
+    z[3 * (size_t)i] = scale * z0;
+    z[3 * (size_t)i + 1] = scale * z1;
+    z[3 * (size_t)i + 2] = scale * z2;
+  }
+}
+void launch_apply_dinv(cudaStream_t st, int nn, const double* dinv, const double* r, double* z, double scale) {
+  k_apply_dinv<<<kVecBlocks, kVecThreads, 0, st>>>(nn, dinv, r, z, scale);
+  CK(cudaGetLastError());
+}
+
+}  // namespace bal

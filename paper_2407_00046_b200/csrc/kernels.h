@@ -1,0 +1,80 @@
+// kernels.h -- launcher declarations shared by the libbal translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bal {
+
+constexpr int kElasticThreads = 128;
+constexpr int kMaxGroups = 64;
+
+// ---- stencils (k_stencils.cu)
+void launch_elastic(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
+                    const double* vol, const double* mu, const double* lam, double* stage, double* grad,
+                    double* lbar);
+void launch_elastic_energy(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
+                           const double* vol, const double* mu, const double* lam, double* out);
+void launch_contact(cudaStream_t st, int n, const double* x, const int* keys, const double* inA,
+                    const double* inAp, const double* mu, const double* s, double sigma, double dhat,
+                    double* stage, double* grad, double* lbar, int* nodes, double* dist, double* dphi);
+void launch_friction(cudaStream_t st, int n, const double* x, const double* xt, const int* keys,
+                     const double* gam, const double* nrm, const double* lam, double chi, double eps,
+                     double* stage, double* grad, double* lbar, int* nodes);
+void launch_friction_energy(cudaStream_t st, int n, const double* x, const double* xt, const int* keys,
+                            const double* gam, const double* nrm, const double* lam, double chi, double eps,
+                            double* out);
+
+// ---- sparse system (k_linalg.cu)
+struct Bsr {
+  int n = 0;             // block rows
+  int nnzb = 0;
+  const int* row_ptr = nullptr;
+  const int* col = nullptr;
+  const double* val = nullptr;
+};
+
+// PCG scalars living in device memory (single group)
+struct PcgScal {
+  double rz, pq, alpha, beta, rr, bnorm, tol, min_old;
+  int k, stop, done, max_iters, window, pad;
+};
+// warm-start per-group scalars
+struct GrpScal {
+  double rz[kMaxGroups], pq[kMaxGroups], alpha[kMaxGroups], beta[kMaxGroups], rr[kMaxGroups],
+      bnorm[kMaxGroups];
+  int active[kMaxGroups], iters[kMaxGroups];
+  int ngroups, max_iters, any_active, pad;
+  double tol;
+};
+
+void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y);
+void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,
+                     double* partials, unsigned* counter, PcgScal* sc);
+void launch_pcg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv,
+                     double* r, double* z, double* p, double* partials, unsigned* counter, PcgScal* sc,
+                     double* hist);
+void launch_pcg_update(cudaStream_t st, int n, const double* dinv, const double* p, const double* q,
+                       double* x, double* r, double* z, double* partials, unsigned* counter, PcgScal* sc,
+                       double* hist);
+void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc);
+
+// warm start (masked SpMV + grouped scalars)
+void launch_spmv_masked(cudaStream_t st, const Bsr& S, const Bsr& C, const int* grp, const double* v,
+                        double* y, const GrpScal* gs);
+void launch_ws_dot(cudaStream_t st, int n, const int* grp, const double* p, const double* q,
+                   double* partials, unsigned* counter, GrpScal* gs);
+void launch_ws_init(cudaStream_t st, int n, const int* grp, const double* b, const double* dinv, double* x,
+                    double* r, double* z, double* p, double* partials, unsigned* counter, GrpScal* gs);
+void launch_ws_update(cudaStream_t st, int n, const int* grp, const double* dinv, const double* p,
+                      const double* q, double* x, double* r, double* z, double* partials, unsigned* counter,
+                      GrpScal* gs);
+void launch_ws_pupdate(cudaStream_t st, int n, const int* grp, const double* z, double* p, const GrpScal* gs);
+
+// generic deterministic reductions
+void launch_dot(cudaStream_t st, int n, const double* a, const double* b, double* partials, double* out);
+void launch_sum(cudaStream_t st, int n, const double* a, double* partials, double* out);
+void launch_min(cudaStream_t st, int n, const double* a, double* partials, double* out);
+void launch_axpy(cudaStream_t st, int n, double alpha, const double* x, const double* y, double* out);
+void launch_apply_dinv(cudaStream_t st, int nn, const double* dinv, const double* r, double* z, double scale);
+
+}  // namespace bal

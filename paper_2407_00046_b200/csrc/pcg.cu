@@ -1,0 +1,182 @@
+// pcg.cu -- host drivers of the warm start (Q20) and the global block-Jacobi PCG with
+// the App. B policy (Q14-Q16).  All scalars stay on the device; the host only polls
+// the device `done` flag once per batch of kBatch iterations (kernels early-exit once done).
+#include <climits>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace bal {
+
+constexpr int kBatch = 8;
+
+__global__ void k_group_minmax(int n, const int* __restrict__ g, int* out /*[2]*/) {
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = g[i];
+    if (v != INT_MIN) {
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+__global__ void k_group_compact(int n, const int* __restrict__ g, int gmin, int G, int* __restrict__ gc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int v = g[i];
+  gc[i] = (v == INT_MIN) ? -1 : min(v - gmin, G - 1);
+}
+
+void compact_groups(bal_ctx* c) {
+  cudaStream_t st = c->st;
+  c->tmp_i.reserve(2);
+  const int init[2] = {INT_MAX, INT_MIN};
+  CK(cudaMemcpyAsync(c->tmp_i.ptr, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  k_group_minmax<<<kRedBlocks, 256, 0, st>>>(c->N, c->group.ptr, c->tmp_i.ptr);
+  int mm[2];
+  CK(cudaMemcpyAsync(mm, c->tmp_i.ptr, sizeof(mm), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int G = (mm[0] == INT_MAX) ? 1 : (mm[1] - mm[0] + 1);
+  // more than kMaxGroups decades cannot occur for finite stiffness; the top decades are merged
+  G = std::min(G, kMaxGroups);
+  c->ngroups = G;
+  k_group_compact<<<ceil_div(c->N, 256), 256, 0, st>>>(c->N, c->group.ptr, mm[0] == INT_MAX ? 0 : mm[0], G,
+                                                       c->grp_c.ptr);
+  CK(cudaGetLastError());
+  c->launches += 2;
+}
+
+static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* stats) {
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  while (true) {
+    for (int it = 0; it < kBatch; ++it) {
+      launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
+      launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
+                        c->counter.ptr, c->scal.ptr, c->hist.ptr);
+      launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
+      c->launches += 3;
+    }
+    CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c->h_scal->done) break;
+  }
+  if (stats) {
+    double rn = 0.0;
+    CK(cudaMemcpy(&rn, c->hist.ptr + c->h_scal->k, sizeof(double), cudaMemcpyDeviceToHost));
+    stats->iters = c->h_scal->k;
+    stats->stop_reason = c->h_scal->stop;
+    stats->rel_residual = c->h_scal->bnorm > 0 ? rn / c->h_scal->bnorm : 0.0;
+  }
+}
+
+int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
+              int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats) {
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  const Bsr S = c->static_bsr(), C = c->contact_bsr();
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if ((int)c->hist.cap < max_iters + 8) c->hist.reserve(max_iters + 8);
+  // ---------------- warm start: per-group PCG on A_GG (Q20)
+  if (warm) {
+    compact_groups(c);
+    GrpScal h;
+    std::memset(&h, 0, sizeof(h));
+    h.ngroups = c->ngroups;
+    h.max_iters = ws_max;
+    h.tol = ws_tol;
+    CK(cudaMemcpyAsync(c->gscal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+    launch_ws_init(st, N, c->grp_c.ptr, rhs, c->dinv.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->partials.ptr,
+                   c->counter.ptr, c->gscal.ptr);
+    c->launches += 1;
+    int done_iters = 0;
+    while (done_iters < ws_max) {
+      const int nb = std::min(kBatch, ws_max - done_iters);
+      for (int it = 0; it < nb; ++it) {
+        launch_spmv_masked(st, S, C, c->grp_c.ptr, c->pp.ptr, c->pq.ptr, c->gscal.ptr);
+        launch_ws_dot(st, N, c->grp_c.ptr, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->gscal.ptr);
+        launch_ws_update(st, N, c->grp_c.ptr, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr,
+                         c->partials.ptr, c->counter.ptr, c->gscal.ptr);
+        launch_ws_pupdate(st, N, c->grp_c.ptr, c->pz.ptr, c->pp.ptr, c->gscal.ptr);
+        c->launches += 4;
+      }
+      done_iters += nb;
+      int any = 0;
+      CK(cudaMemcpyAsync(&any, &c->gscal.ptr->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!any) break;
+    }
+    if (stats) {
+      GrpScal g;
+      CK(cudaMemcpyAsync(&g, c->gscal.ptr, sizeof(g), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      int mx = 0;
+      for (int i = 0; i < g.ngroups; ++i) mx = std::max(mx, g.iters[i]);
+      stats->ws_iters_max = mx;
+      stats->n_groups = g.ngroups;
+    }
+    // x0 := warm-start result (already in px)
+  } else if (x0) {
+    CK(cudaMemcpyAsync(c->px.ptr, x0, 3 * (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(cudaMemsetAsync(c->px.ptr, 0, 3 * (size_t)N * sizeof(double), st));
+  }
+  // ---------------- global PCG from x0
+  PcgScal h;
+  std::memset(&h, 0, sizeof(h));
+  h.tol = tol;
+  h.window = window;
+  h.max_iters = max_iters;
+  CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
+  launch_pcg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->partials.ptr, c->counter.ptr,
+                  c->scal.ptr, c->hist.ptr);
+  c->launches += 2;
+  CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int ws_it = stats ? stats->ws_iters_max : 0, ng = stats ? stats->n_groups : 0;
+  if (!c->h_scal->done) run_batches(c, S, C, stats);
+  else if (stats) {
+    stats->iters = 0;
+    stats->stop_reason = c->h_scal->stop;
+    stats->rel_residual = c->h_scal->bnorm > 0 ? std::sqrt(c->h_scal->rr) / c->h_scal->bnorm : 0.0;
+  }
+  if (stats) {
+    stats->ws_iters_max = ws_it;
+    stats->n_groups = ng;
+  }
+  if (x_out && x_out != c->px.ptr)
+    CK(cudaMemcpyAsync(x_out, c->px.ptr, 3 * (size_t)N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return c->h_scal->k;
+}
+
+// App. B: "return to the PCG method for an additional 100 iterations" from the saved state.
+__global__ void k_set_resume(PcgScal* sc, int extra, int cap) {
+  sc->tol = 0.0;
+  sc->window = 0;
+  sc->max_iters = min(sc->k + extra, cap);
+  sc->done = (sc->k >= sc->max_iters) ? 1 : 0;
+  sc->stop = -1;
+}
+
+void pcg_resume(bal_ctx* c, int extra, double* x_out, bal_pcg_stats* stats) {
+  cudaStream_t st = c->st;
+  k_set_resume<<<1, 1, 0, st>>>(c->scal.ptr, extra, c->prm.max_pcg);
+  c->launches += 1;
+  const Bsr S = c->static_bsr(), C = c->contact_bsr();
+  CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (!c->h_scal->done) run_batches(c, S, C, stats);
+  if (x_out && x_out != c->px.ptr)
+    CK(cudaMemcpyAsync(x_out, c->px.ptr, 3 * (size_t)c->N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+}
+
+}  // namespace bal

@@ -1,0 +1,108 @@
+"""GPU step parity: bal_step (CUDA, through the C ABI) vs oracle.bal.Oracle.step on identical seeded
+scenes (SURVEY.md §8(c) c.4 "Step"), plus non-penetration and run-to-run determinism."""
+import numpy as np
+import pytest
+
+import scenes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2407_00046_b200 as bal  # noqa: E402
+from oracle import contact as cm  # noqa: E402
+from oracle.bal import Oracle  # noqa: E402
+from oracle.energy import nh_min_J  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def gpu_steps(sc, nsteps, flags=0):
+    ctx = bal.bal_init(sc, flags=flags)
+    x = torch.as_tensor(sc["x0"].ravel(), device=DEV)
+    v = torch.as_tensor(sc["v0"].ravel(), device=DEV)
+    xs, traces, stats = [], [], []
+    for _ in range(nsteps):
+        xn = torch.empty_like(x)
+        vn = torch.empty_like(v)
+        s = bal.bal_step(ctx, x, v, xn, vn)
+        traces.append(bal.bal_get_trace(ctx))
+        stats.append(s)
+        x, v = xn, vn
+        xs.append(x.cpu().numpy().reshape(-1, 3).copy())
+    return xs, traces, stats
+
+
+def oracle_steps(sc, nsteps, flags=0):
+    o = Oracle(sc, flags=flags)
+    x, v = sc["x0"], sc["v0"]
+    xs, traces = [], []
+    for _ in range(nsteps):
+        tr = []
+        x, v, _ = o.step(x, v, tr)
+        xs.append(x.copy())
+        traces.append(tr)
+    return xs, traces
+
+
+def _rel(a, b, ref):
+    return np.linalg.norm(a - b) / np.linalg.norm(ref)
+
+
+def test_tet_drop_parity():
+    sc = scenes.make_single_tet(1, height=0.01, speed=1.0)
+    xg, tg, _ = gpu_steps(sc, 4)
+    xo, to = oracle_steps(sc, 4)
+    for k in range(4):
+        assert _rel(xg[k], xo[k], xo[k] - sc["x0"]) <= 1e-6, k
+        assert len(tg[k]) == len(to[k])
+
+
+def test_cubes_ten_step_parity():
+    """C1 (BASELINE configs[0]): positions within 1e-6 relative after each of 10 steps."""
+    sc = scenes.make_cubes(1)
+    xg, tg, sg = gpu_steps(sc, 10)
+    xo, to = oracle_steps(sc, 10)
+    errs = [np.linalg.norm(xg[k] - xo[k]) / np.linalg.norm(xo[k]) for k in range(10)]
+    disp = [np.linalg.norm(xg[k] - xo[k]) / np.linalg.norm(xo[k] - sc["x0"]) for k in range(10)]
+    print("rel position error per step:", ["%.1e" % e for e in errs])
+    print("rel displacement error per step:", ["%.1e" % e for e in disp])
+    print("newton iters gpu/oracle:", [(len(a), len(b)) for a, b in zip(tg, to)])
+    assert max(errs) <= 1e-6
+
+
+def test_gpu_steps_are_intersection_free_and_deterministic():
+    sc = scenes.make_cubes(1)
+    xa, _, _ = gpu_steps(sc, 3)
+    xb, _, _ = gpu_steps(sc, 3)
+    for a, b in zip(xa, xb):
+        assert np.array_equal(a, b)  # atomic-free, fixed-order reductions: bitwise deterministic
+    o = Oracle(sc)
+    prev = sc["x0"]
+    for x in xa:
+        pt, ee = cm.candidates(o.mesh, prev, x, o.dhat)
+        for ts in np.linspace(0, 1, 51):
+            xs = prev + ts * (x - prev)
+            for ftype, pairs in ((cm.PT, pt), (cm.EE, ee)):
+                if len(pairs):
+                    D, _, _ = cm.resolve_features(xs, ftype, pairs)
+                    assert D.min() > 0.0
+        assert nh_min_J(x, o.mesh) > 0
+        prev = x
+
+
+def test_free_fall_on_gpu():
+    sc = scenes.make_free_cube(3)
+    xg, _, _ = gpu_steps(sc, 1)
+    y = sc["x0"] + sc["params"]["h"] * sc["v0"] + sc["params"]["h"] ** 2 * np.array(sc["params"]["gravity"])
+    assert np.linalg.norm(xg[0] - y) <= 1e-6 * np.linalg.norm(y - sc["x0"])
+
+
+def test_step_host_matches_device_step():
+    sc = scenes.make_single_tet(1, height=0.01, speed=1.0)
+    ctx = bal.bal_init(sc)
+    xh, vh, _ = bal.bal_step_host(ctx, sc["x0"], sc["v0"])
+    xg, _, _ = gpu_steps(sc, 1)
+    assert np.array_equal(xh.reshape(-1, 3), xg[0])
