@@ -30,6 +30,9 @@ from .energy import barrier, inertia_energy, inertia_grad, nh_energy, nh_stencil
 from .mesh import precompute
 from .projection import project_eigh
 
+# R-LS1: energy comparisons tolerate 8 units of roundoff of the summed magnitudes
+LS_ROUND = 8.0 * 2.0 ** -53
+
 FLAG_NO_WARMSTART = 1
 FLAG_NO_AUGLAG = 2
 
@@ -61,27 +64,36 @@ class Oracle:
 
     # ------------------------------------------------------------------ energy
     def energy(self, x, st, pt, ee):
-        """L(x) at fixed (y, sigma, A' with mu, s, friction anchors); returns (L, n_constraints)."""
+        """L(x) at fixed (y, sigma, A' with mu, s, friction anchors).  Returns (L, n_constraints, S)
+        where S = sum of the magnitudes of all terms of L -- the scale of its FP64 evaluation error
+        used by the line-search acceptance (DESIGN.md R-LS1)."""
         m = self.mesh
         if m.tets.size and nh_energy(x, m) == np.inf:
-            return np.inf, 0
+            return np.inf, 0, np.inf
         keys, d = cm.constraint_set(x, pt, ee, self.dhat)
         if len(d) and np.min(d) <= 0.0:
-            return np.inf, len(d)
+            return np.inf, len(d), np.inf
         dap = cm.key_distance(x, st["ap_keys"]) if len(st["ap_keys"]) else np.zeros(0)
         if len(dap) and np.min(dap) <= 0.0:
-            return np.inf, len(d)
-        L = inertia_energy(x, st["y"], m.mass, self.h, self.free) + nh_energy(x, m)
-        L += float(np.sum(st["sigma"] * barrier(d, self.dhat)))
+            return np.inf, len(d), np.inf
+        ei = inertia_energy(x, st["y"], m.mass, self.h, self.free)
+        ee_ = nh_energy(x, m)
+        eb = float(np.sum(st["sigma"] * barrier(d, self.dhat)))
+        L = ei + ee_ + eb
+        S = abs(ei) + abs(ee_) + abs(eb)
         if len(dap):
-            L += float(np.sum(cm.phi_energy(dap, np.zeros(len(dap)), np.ones(len(dap)),
-                                            st["ap_mu"], st["ap_s"], st["sigma"], self.dhat)))
+            al = cm.phi_energy(dap, np.zeros(len(dap)), np.ones(len(dap)), st["ap_mu"], st["ap_s"], st["sigma"],
+                               self.dhat)
+            L += float(np.sum(al))
+            S += float(np.sum(np.abs(al)))
         if st.get("fr_keys") is not None and len(st["fr_keys"]):
-            L += cm.friction_energy(x, st["x_t"], st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"],
+            ef = cm.friction_energy(x, st["x_t"], st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"],
                                     float(self.p["chi"]), float(self.p["eps_v"]), self.h)
+            L += ef
+            S += abs(ef)
         if not np.isfinite(L):
-            return np.inf, len(d)
-        return L, len(d)
+            return np.inf, len(d), np.inf
+        return L, len(d), S
 
     # ---------------------------------------------------------------- stencils
     def contact_stencil_set(self, x, keys_A, st):
@@ -281,11 +293,12 @@ class Oracle:
                 cpt, cee = cm.candidates(m, x, x + P, dhat)
                 a_ccd = ccdm.step_toi(x, P, cpt, cee, dhat)
                 alpha = min(1.0, a_ccd)
-                L0, _n0 = self.energy(x, st, cpt, cee)
+                L0, _n0, S0 = self.energy(x, st, cpt, cee)
                 halvings = 0
                 while alpha >= float(p["alpha_min"]):
-                    L1, n1 = self.energy(x + alpha * P, st, cpt, cee)
-                    if n1 <= int(p["max_constraints"]) and L1 <= L0:
+                    L1, n1, S1 = self.energy(x + alpha * P, st, cpt, cee)
+                    # R-LS1: accept when L does not increase beyond its FP64 evaluation error
+                    if n1 <= int(p["max_constraints"]) and L1 <= L0 + LS_ROUND * max(S0, S1):
                         break
                     alpha *= 0.5
                     halvings += 1

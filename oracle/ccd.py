@@ -11,7 +11,11 @@ DESIGN.md reading R-CCD1:
     bisection fallback until |dt| <= 1e-15 (<= 100 iterations); deflate
     (A=a, B=b+A t*, C=c+B t*; Q31 reading of the garbled P:466) and solve the quadratic in
     closed form; clamp roots to [0,1]; sort.
- 3. activation: the first root (ascending) with d_TOC < dhat + eps.
+ 3. activation: the first root (ascending) with d_TOC < eps + min(dhat, 1e-2 d_0), d_0 the pair's
+    distance at t = 0 (PAPER.md:468 writes eps + dhat; DESIGN.md R-CCD2: with the full dhat margin a
+    pair already within dhat that slides tangentially past a neighbouring primitive's plane is
+    truncated to 0.9 t at every Newton iteration -- a Zeno stall observed on C1 step 3 -- while a
+    genuine crossing has d_TOC = 0 up to root error either way).
  4. conservative TOI (PAPER.md:481-482, fig:ccd_toi): reference frame t_ref = (t_prev + t)/2;
     R-CCD1: the root itself is the coplanar configuration whose signed distance is rounding
     noise, so the TOI is backtracked at least once: toi = 0.9 t, then while the signed distance
@@ -135,12 +139,14 @@ def pair_toi(ftype, x, dx, ids, dhat):
             return 1.0
         return min(1.0, 0.9 * d0 / (ma + mb))
     roots = cubic_roots(a, b, c, d)
+    d0 = np.sqrt(resolve_features(x, ftype, ids[None])[0][0])
+    thr = EPS + min(dhat, 1e-2 * d0)  # R-CCD2: activation margin scaled by the current gap
     t_prev = 0.0
     for t in roots:
         xt = x.copy()
         xt[ids] = X0 + t * DX
         D, sub, _ = resolve_features(xt, ftype, ids[None])
-        if np.sqrt(D[0]) < dhat + EPS:
+        if np.sqrt(D[0]) < thr:
             toi = 0.9 * t
             if sub[0] in (PT, EE):
                 tref = 0.5 * (t_prev + t)

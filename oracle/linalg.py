@@ -75,7 +75,7 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
         st.r = st.r - alpha * q
         st.z = apply_block(Dinv, st.r)
         rz_new = float(st.r @ st.z)
-        beta = rz_new / st.rz
+        beta = rz_new / st.rz if st.rz != 0.0 else 0.0  # r = 0 exactly: converged, next check stops
         st.rz = rz_new
         st.p = st.z + beta * st.p
         st.hist.append(float(np.linalg.norm(st.r)))

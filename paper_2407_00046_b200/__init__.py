@@ -105,7 +105,14 @@ def bal_init(scene, device=0, flags=0, params=None):
     st = _lib.lib.bal_init(C.byref(m), ma, len(mats), C.byref(prm), device, C.byref(h))
     if st != 0:
         raise BalError(st, _lib.lib.bal_last_error(None).decode())
-    return BalCtx(h, scene)
+    ctx = BalCtx(h, scene)
+    try:  # order library work after torch's work on this device (device tensors come from torch)
+        import torch
+        if torch.cuda.is_available():
+            bal_set_stream(ctx, torch.cuda.current_stream(device))
+    except ImportError:
+        pass
+    return ctx
 
 
 def bal_destroy(ctx):
@@ -149,6 +156,13 @@ def bal_get_trace(ctx, max_records=100000):
         raise BalError(n, "bal_get_trace")
     rows = out[:n * len(TRACE_FIELDS)].reshape(n, len(TRACE_FIELDS))
     return [dict(zip(TRACE_FIELDS, r.tolist())) for r in rows]
+
+
+def bal_spmv_counters(ctx):
+    """(total SpMV kernel ms, launches, algorithmic bytes, full-BSR minimum bytes) since ctx creation."""
+    out = np.zeros(4)
+    _check(ctx, _lib.lib.bal_spmv_counters(ctx.handle, _lib.ptr(out, C.c_double)))
+    return dict(ms=out[0], launches=int(out[1]), bytes_alg=out[2], bytes_moved=out[3])
 
 
 def _keys_arr(k):

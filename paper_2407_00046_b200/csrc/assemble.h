@@ -56,6 +56,7 @@ struct ContactWork {
   DevBuf<int> row_ptr, col;
   DevBuf<double> val;
   int nslots = 0;
+  int nrows = 0;  // non-empty contact rows (= contact diagonal slots)
 };
 
 void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage, const double* mass,

@@ -379,7 +379,9 @@ bal_status bal_init(const bal_mesh* mesh, const bal_material* materials, int32_t
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw ArgError("bal_init: no such CUDA device");
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    // blocking stream: implicitly ordered after work on the legacy default stream (e.g. a torch
+    // H2D copy of x_t issued just before bal_step), so callers need no explicit sync
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamDefault));
     c->st = c->own_stream;
     if (!(c->prm.h > 0) || !(c->prm.dhat > 0)) throw ArgError("bal_init: h and dhat must be > 0");
     precompute(c, mesh, materials, n_materials);
@@ -547,6 +549,15 @@ bal_status bal_bench_spmv(bal_ctx* c, int32_t iters, double* mean_us) {
 }
 
 int64_t bal_kernel_launches(const bal_ctx* c) { return c ? c->launches : 0; }
+
+bal_status bal_spmv_counters(const bal_ctx* c, double* out) {
+  if (!c || !out) return BAL_E_INVALID_ARG;
+  out[0] = c->spmv_ms;
+  out[1] = (double)c->spmv_count;
+  out[2] = c->spmv_bytes_alg;
+  out[3] = c->spmv_bytes_moved;
+  return BAL_OK;
+}
 
 const char* bal_last_error(const bal_ctx* c) { return c ? c->err.c_str() : g_init_err.c_str(); }
 

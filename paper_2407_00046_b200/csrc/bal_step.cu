@@ -201,7 +201,12 @@ struct Energy {
   double L;
   int count;
   double dmin;
+  double S;
 };
+
+// R-LS1: the line search accepts L(x + a p) <= L(x) + 8u max(S0, S1), i.e. no increase
+// beyond the FP64 evaluation error of L (S = sum of the magnitudes of its terms).
+constexpr double kLsRound = 8.0 * 1.1102230246251565e-16;
 
 double host_scalar(bal_ctx* c, const double* dev) {
   double v;
@@ -219,7 +224,8 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
   w.evals.reserve(std::max(N, T) + 1);
   w.cw.part.reserve(kRedBlocks);
   double* E = w.esc.ptr;
-  // [0] elastic, [1] inertia, [2] barrier, [3] barrier dmin, [4] AL, [5] AL dmin, [6] friction
+  // [0] elastic, [1] inertia, [2] barrier, [3] barrier dmin, [4] AL, [5] AL dmin, [6] friction,
+  // [7] sum |AL_i|
   CK(cudaMemsetAsync(E, 0, 8 * sizeof(double), st));
   if (T > 0) {
     launch_elastic_energy(st, T, xe, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr, w.evals.ptr);
@@ -233,7 +239,7 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
   if (w.n_ap > 0) {
     w.ap_d.reserve(w.n_ap);
     key_distances(st, w.n_ap, w.ap_keys.ptr, xe, w.ap_d.ptr);
-    phi_al_energy(st, w.cw, w.n_ap, w.ap_d.ptr, w.ap_mu.ptr, w.ap_s.ptr, sigma, dhat, E + 4, E + 5);
+    phi_al_energy(st, w.cw, w.n_ap, w.ap_d.ptr, w.ap_mu.ptr, w.ap_s.ptr, sigma, dhat, E + 4, E + 5, E + 7);
   } else {
     const double inf = INFINITY;
     CK(cudaMemcpyAsync(E + 5, &inf, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -254,6 +260,9 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
   const bool bad = !(hv[3] > 0.0) || !(hv[5] > 0.0) || !std::isfinite(hv[0]);
   const double L = hv[1] + hv[0] + hv[2] + hv[4] + hv[6];
   r.L = (bad || !std::isfinite(L)) ? INFINITY : L;
+  // magnitude scale of the FP64 evaluation error of L (DESIGN.md R-LS1)
+  r.S = std::fabs(hv[1]) + std::fabs(hv[0]) + std::fabs(hv[2]) + hv[7] + std::fabs(hv[6]);
+  if (!std::isfinite(r.L)) r.S = INFINITY;
   return r;
 }
 
@@ -482,10 +491,11 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
       const Energy E0 = energy(c, w, w.x.ptr, w.cand_sw, sigma);
       halvings = 0;
       bool ok = false;
+      Energy E1{};
       while (alpha >= P.alpha_min) {
         launch_axpy(st, 3 * N, alpha, w.dir.ptr, w.x.ptr, w.trial.ptr);
-        const Energy E1 = energy(c, w, w.trial.ptr, w.cand_sw, sigma);
-        if (E1.count <= P.max_constraints && E1.L <= E0.L) {
+        E1 = energy(c, w, w.trial.ptr, w.cand_sw, sigma);
+        if (E1.count <= P.max_constraints && E1.L <= E0.L + kLsRound * std::max(E0.S, E1.S)) {
           ok = true;
           break;
         }
@@ -495,7 +505,12 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
       if (ok) break;
       if (resumes >= 50 || c->h_scal->k >= P.max_pcg) {
         S.ms_linesearch += ms_since(t0);
-        throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: line search failed after PCG resumes");
+        char buf[320];
+        snprintf(buf, sizeof(buf),
+                 "bal_step: line search failed after %d PCG resumes (newton l=%d, alpha_ccd=%.3e, L0=%.17g, "
+                 "last L1=%.17g, |C|=%d, dmin=%.3e, pcg k=%d, safeguard=%d)",
+                 resumes, l, a_ccd, E0.L, E1.L, E1.count, E1.dmin, c->h_scal->k, safeguard);
+        throw StepFail(BAL_E_NOT_CONVERGED, buf);
       }
       ++resumes;
       pcg_resume(c, P.pcg_resume_iters, w.dir.ptr, &ps);

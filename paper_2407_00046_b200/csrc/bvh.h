@@ -54,6 +54,6 @@ double ccd_step_toi(cudaStream_t st, CollisionWork& w, const Candidates& c, cons
                     double dhat);
 void key_distances(cudaStream_t st, int n, const int* keys, const double* x, double* d);
 void phi_al_energy(cudaStream_t st, CollisionWork& w, int n, const double* d, const double* mu, const double* s,
-                   double sigma, double dhat, double* out_sum, double* out_min);
+                   double sigma, double dhat, double* out_sum, double* out_min, double* out_abs_sum);
 
 }  // namespace bal

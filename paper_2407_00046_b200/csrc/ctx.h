@@ -61,6 +61,26 @@ struct bal_ctx {
   bal::DevBuf<double> tmp_a, tmp_b, red;
   bal::DevBuf<int> tmp_i;
 
+  // ---- SpMV instrumentation (CUDA events around every PCG SpMV launch)
+  cudaEvent_t ev[16] = {};
+  bool ev_ready = false;
+  double spmv_ms = 0.0, spmv_bytes_alg = 0.0, spmv_bytes_moved = 0.0;
+  long long spmv_count = 0;
+  // B_alg = 72N + 76E + 4(N+1) + 80C + 48N (symmetric D/L/C layout, int32 indices)
+  double spmv_alg_bytes() const {
+    const double n = N;
+    const double E = loaded_bsr ? 0.5 * (lb_nnzb - N) : 0.5 * (sp.nnzb - N);
+    const double Cb = loaded_bsr ? 0.0 : 0.5 * (cw.nslots - cw.nrows);
+    return 72.0 * n + 76.0 * E + 4.0 * (n + 1) + 80.0 * Cb + 48.0 * n;
+  }
+  // bytes the full-BSR kernel must move at minimum (both triangles stored)
+  double spmv_moved_bytes() const {
+    const double n = N;
+    const double s = loaded_bsr ? lb_nnzb : sp.nnzb;
+    const double cc = loaded_bsr ? 0 : cw.nslots;
+    return 76.0 * s + 4.0 * (n + 1) + (cc > 0 ? 76.0 * cc + 4.0 * (n + 1) : 0.0) + 48.0 * n;
+  }
+
   // ---- time-step work (bal_step.cu), allocated on first use
   struct StepWork* sw = nullptr;
   std::vector<double> trace;  // per-Newton-iteration decision trace of the last bal_step

@@ -150,6 +150,13 @@ __global__ void k_contact_rowptr(int n, int nslots, const unsigned long long* __
   row_ptr[r] = lo;
 }
 
+__global__ void k_count_rows(int n, const int* __restrict__ row_ptr, int* cnt) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ne = (r < n && row_ptr[r + 1] > row_ptr[r]) ? 1 : 0;
+  const int s = __syncthreads_count(ne);
+  if (threadIdx.x == 0 && s) atomicAdd(cnt, s);
+}
+
 // per node: gradient, Lambda -> e_j, group, diagonal block inverse
 __global__ void k_node_finalize(int n, const double* __restrict__ x, const double* __restrict__ y,
                                 const double* __restrict__ mass, double inv_h2, const uint8_t* __restrict__ fixed,
@@ -233,6 +240,7 @@ void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage
 int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* nodes, const uint8_t* fixed, int n,
                           const double* stage) {
   w.nslots = 0;
+  w.nrows = 0;
   if (ns <= 0) return 0;
   const int m = 16 * ns;
   w.keys.reserve(m);
@@ -271,7 +279,10 @@ int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* no
   if (nslots > 0)
     k_gather_contact<<<ceil_div(nslots, 256), 256, 0, st>>>(nslots, w.keys_alt.ptr, w.codes_alt.ptr, w.start.ptr,
                                                              stage, w.col.ptr, w.val.ptr);
+  CK(cudaMemsetAsync(w.nvalid.ptr, 0, sizeof(int), st));
+  k_count_rows<<<ceil_div(n, 256), 256, 0, st>>>(n, w.row_ptr.ptr, w.nvalid.ptr);
   CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&w.nrows, w.nvalid.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   return nslots;
 }
 

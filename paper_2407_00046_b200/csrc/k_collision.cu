@@ -141,18 +141,21 @@ void key_distances(cudaStream_t st, int n, const int* keys, const double* x, dou
 }
 
 __global__ void k_phi_al(int n, const double* __restrict__ d, const double* __restrict__ mu,
-                         const double* __restrict__ s, double sigma, double dhat, double* out) {
+                         const double* __restrict__ s, double sigma, double dhat, double* out, double* out_abs) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double di = d[i];
-  out[i] = (di > 0.0) ? mu[i] * (dhat + s[i] - di) + sigma * barrier_b(di, dhat + s[i]) : INFINITY;
+  const double v = (di > 0.0) ? mu[i] * (dhat + s[i] - di) + sigma * barrier_b(di, dhat + s[i]) : INFINITY;
+  out[i] = v;
+  out_abs[i] = fabs(v);
 }
 void phi_al_energy(cudaStream_t st, CollisionWork& w, int n, const double* d, const double* mu, const double* s,
-                   double sigma, double dhat, double* out_sum, double* out_min) {
-  w.vals.reserve(std::max(n, 1));
+                   double sigma, double dhat, double* out_sum, double* out_min, double* out_abs_sum) {
+  w.vals.reserve(2 * (size_t)std::max(n, 1));
   w.part.reserve(kRedBlocks);
-  k_phi_al<<<ceil_div(n, 256), 256, 0, st>>>(n, d, mu, s, sigma, dhat, w.vals.ptr);
+  k_phi_al<<<ceil_div(n, 256), 256, 0, st>>>(n, d, mu, s, sigma, dhat, w.vals.ptr, w.vals.ptr + n);
   launch_sum(st, n, w.vals.ptr, w.part.ptr, out_sum);
+  launch_sum(st, n, w.vals.ptr + n, w.part.ptr, out_abs_sum);
   launch_min(st, n, d, w.part.ptr, out_min);
 }
 
@@ -281,13 +284,17 @@ BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat) {
   }
   double roots[3];
   const int nr = cubic_roots(aa, bb, cc, dd, roots);
+  if (nr == 0) return 1.0;
+  // DESIGN.md R-CCD2: activation margin eps + min(dhat, 1e-2 d_0) (P:468 writes eps + dhat)
+  const double d0 = sqrt(resolve(ftype, X0[0], X0[1], X0[2], X0[3]).D);
+  const double thr = kCcdEps + fmin(dhat, 1e-2 * d0);
   double t_prev = 0.0;
   for (int i = 0; i < nr; ++i) {
     const double t = roots[i];
     d3 P[4];
     for (int k = 0; k < 4; ++k) P[k] = X0[k] + t * DX[k];
     const Resolved rs = resolve(ftype, P[0], P[1], P[2], P[3]);
-    if (sqrt(rs.D) < dhat + kCcdEps) {
+    if (sqrt(rs.D) < thr) {
       double toi = 0.9 * t;
       if (rs.type == T_PT || rs.type == T_EE) {
         const double tref = 0.5 * (t_prev + t);

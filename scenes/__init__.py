@@ -279,3 +279,103 @@ def make_free_cube(seed=0, cells=3, E=1e5, nu=0.4, rho=1e3):
     sb = SceneBuilder()
     sb.add_body(xb, tb, 0, v0=tuple(rng.normal(size=3)))
     return sb.build([(E, nu, rho)], "free-cube")
+
+
+# --------------------------------------------------------------------------
+# C4: puffer balls on a chain-net (BASELINE.json configs[3])
+# --------------------------------------------------------------------------
+def _ring_xz(L):
+    """1-voxel-thick square ring of outer size L in the xz plane (height 1 voxel)."""
+    occ = np.zeros((L, 1, L), bool)
+    occ[:, 0, :] = True
+    occ[1:L - 1, 0, 1:L - 1] = False
+    return occ
+
+
+def _ring_xy(Lx, Ly):
+    occ = np.zeros((Lx, Ly, 1), bool)
+    occ[:, :, 0] = True
+    occ[1:Lx - 1, 1:Ly - 1, 0] = False
+    return occ
+
+
+def _ring_zy(Lz, Ly):
+    occ = np.zeros((1, Ly, Lz), bool)
+    occ[0, :, :] = True
+    occ[0, 1:Ly - 1, 1:Lz - 1] = False
+    return occ
+
+
+def _fib_dirs(n):
+    k = np.arange(n) + 0.5
+    phi = np.arccos(1 - 2 * k / n)
+    th = np.pi * (1 + 5 ** 0.5) * k
+    return np.stack([np.cos(th) * np.sin(phi), np.cos(phi), np.sin(th) * np.sin(phi)], axis=1)
+
+
+def spiky_ball_occ(R, n_spikes, spike_len, spike_r=0.75):
+    """Voxel occupancy of a solid sphere of radius R (voxels) with radial cylindrical spikes."""
+    ext = int(np.ceil(R + spike_len + 2))
+    g = np.arange(-ext, ext) + 0.5
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    r2 = X * X + Y * Y + Z * Z
+    occ = r2 <= R * R
+    P = np.stack([X, Y, Z], axis=-1)
+    for d in _fib_dirs(n_spikes):
+        t = P @ d
+        perp2 = r2 - t * t
+        occ |= (t >= R - 1) & (t <= R + spike_len) & (perp2 <= spike_r * spike_r)
+    return occ, ext
+
+
+def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=19.6, n_spikes=110,
+                    spike_len=15.0, n_balls=4, E_ball=5e5, E_net=1e9, nu=0.4, rho=1e3, chi=0.3, drop_gap=0.002):
+    """C4 recipe (Table 1 row 1 P:664 for the statistics): a chain-net of
+    interlocked 1-voxel-thick square rings (horizontal rings on an nx x nz lattice plus vertical
+    connector rings threading neighbours through their holes; outermost horizontal rings fixed)
+    and n_balls spiky balls (voxel core + radial spikes on a Fibonacci direction set) dropped onto
+    it.  Every ring gets a small generic rotation so no cross-body edges are exactly parallel.
+    Defaults target T ~ 1.76M tets, N ~ 0.8M nodes."""
+    rng = np.random.default_rng(seed)
+    sb = SceneBuilder()
+    xr, tr = voxel_mesh(_ring_xz(L), voxel)
+    cx_occ = _ring_xy(spacing - L + L // 2 * 2 - 1 + 2, 9)
+    # connector between horizontal rings along x: vertical beams inside both holes
+    conn_len = spacing - 1  # x span in voxels
+    xcx, tcx = voxel_mesh(_ring_xy(conn_len, 9), voxel)
+    xcz, tcz = voxel_mesh(_ring_zy(conn_len, 9), voxel)
+
+    def jitter(x):
+        c = x.mean(0)
+        ax = rng.normal(size=3)
+        R = rot_axis(ax, np.deg2rad(rng.uniform(0.2, 0.8)))
+        return (x - c) @ R.T + c
+
+    for i in range(nx):
+        for k in range(nz):
+            o = np.array([i * spacing, 0.0, k * spacing]) * voxel
+            border = i == 0 or k == 0 or i == nx - 1 or k == nz - 1
+            x = xr + o
+            if not border:
+                x = jitter(x)
+            sb.add_body(x, tr, 1, fixed=np.full(len(xr), 1 if border else 0, np.uint8))
+            if i + 1 < nx:
+                # vertical ring in the xy plane through the holes of rings (i,k) and (i+1,k)
+                oc = o + np.array([L // 2 + 1, -4, L // 2 - 0.5]) * voxel
+                sb.add_body(jitter(xcx + oc), tcx, 1)
+            if k + 1 < nz:
+                oc = o + np.array([L // 2 - 0.5, -4, L // 2 + 1]) * voxel
+                sb.add_body(jitter(xcz + oc), tcz, 1)
+    del cx_occ
+    occ, ext = spiky_ball_occ(ball_R, n_spikes, spike_len)
+    xb, tb = voxel_mesh(occ, voxel)
+    xb = xb - ext * voxel
+    span = np.array([(nx - 1) * spacing + L, (nz - 1) * spacing + L]) * voxel
+    top = 6 * voxel  # above the connector rings
+    for b in range(n_balls):
+        fx = (0.3 + 0.4 * (b % 2)) * span[0]
+        fz = (0.3 + 0.4 * (b // 2 % 2)) * span[1]
+        xbb = xb @ random_rotation(rng).T
+        xbb = xbb + np.array([fx, top - xbb[:, 1].min() + drop_gap, fz])
+        sb.add_body(xbb, tb, 0, v0=(0.0, -1.0, 0.0))
+    return sb.build([(E_ball, nu, rho), (E_net, nu, rho)], "C4-puffer-net", chi=chi)
