@@ -209,6 +209,10 @@ typedef struct {
 } bal_bsr_host;
 bal_status bal_load_bsr(bal_ctx* ctx, const bal_bsr_host* bsr);
 
+/* Residual history ||r_k||, k = 0..iters, of the last global PCG solve (HOST out[max_n]);
+ * returns the number of entries written (or a negative bal_status). */
+int32_t bal_pcg_history(bal_ctx* ctx, double* out, int32_t max_n);
+
 /* Timing helper for the benchmark: run `iters` SpMV launches on the current system with CUDA
  * events on the ctx stream; returns the mean launch duration in microseconds. */
 bal_status bal_bench_spmv(bal_ctx* ctx, int32_t iters, double* mean_us);

@@ -146,16 +146,18 @@ class Oracle:
         # contact
         uk, inA, inAp, mu, s = self.contact_stencil_set(x, keys_A, st)
         cs = cm.contact_stencils(x, uk, inA, inAp, mu, s, st["sigma"], self.dhat) if len(uk) else []
-        c_P, c_lb = [], []
+        c_P, c_lb, c_ids = [], [], []
         for (ids, g, H, _d, _dp) in cs:
             P, wc = project_eigh(H[None])
-            lb = wc.sum() / (3 * len(ids))
+            lb = wc.sum() / (3 * len(ids))  # Q18 over the stencil's support nodes (R-DUP1)
             grad.reshape(N, 3)[ids] += g.reshape(-1, 3)
             lam_diag[ids] += lb
             _coo_add(rows, cols, vals, ids, P[0])
             c_P.append(P[0])
             c_lb.append(lb)
+            c_ids.append(ids)
         out["contact_keys"], out["contact_P"], out["contact_lbar"] = uk, c_P, c_lb
+        out["contact_ids"] = c_ids
         out["contact_inA"], out["contact_inAp"] = inA, inAp
         # friction (PSD analytically; not projected, not in Lambda: Q17)
         if st.get("fr_keys") is not None and len(st["fr_keys"]):

@@ -225,26 +225,32 @@ def candidates(mesh, xa, xb, inflate):
 
 
 def constraint_set(x, pt, ee, dhat):
-    """Unique resolved constraints with d < dhat among the candidate feature pairs.
+    """Active constraints: the candidate feature pairs (vertex-triangle, edge-edge) whose feature
+    distance is < dhat (PAPER.md:147-156 "i-th primitive pair in the active primitive set").
+    DESIGN.md R-DUP1: every feature pair is its own constraint with its own (continuous) feature
+    distance; degenerate duplicates (two vertex-triangle pairs resolving to the same point-edge) are
+    NOT merged, because merging makes the barrier sum jump when the vertex slides from the shared
+    edge onto one triangle (SURVEY Q28 reading replaced).  Key = [PT|EE, role-ordered ids].
     Returns (keys (M,5) sorted lexicographically, d (M,))."""
     rows, ds = [], []
     for ftype, pairs in ((PT, pt), (EE, ee)):
         if len(pairs) == 0:
             continue
-        D, typ, loc = resolve_features(x, ftype, pairs)
+        D, _typ, _loc = resolve_features(x, ftype, pairs)
         m = D < dhat * dhat
         if not np.any(m):
             continue
-        loc = loc[m]
-        g = np.where(loc >= 0, np.take_along_axis(pairs[m], np.maximum(loc, 0), axis=1), -1)
-        rows.append(canonical_keys(typ[m], g))
+        k = np.empty((int(m.sum()), 5), np.int64)
+        k[:, 0] = ftype
+        k[:, 1:] = pairs[m]
+        rows.append(k)
         ds.append(np.sqrt(D[m]))
     if not rows:
         return np.zeros((0, 5), np.int64), np.zeros(0)
     keys = np.concatenate(rows)
     d = np.concatenate(ds)
-    keys, idx = np.unique(keys, axis=0, return_index=True)
-    d = d[idx]
+    order = np.lexsort(keys.T[::-1])
+    keys, d = keys[order], d[order]
     m = d < dhat
     return keys[m], d[m]
 
@@ -291,27 +297,29 @@ def _sqdist_ad(sub, P):
 
 
 def contact_stencils(x, keys, inA, inAp, mu, s, sigma, dhat):
-    """Gradient and (unprojected) Hessian of phi_i(d_i(x)) for each key (Q22).
-    Returns list of (node ids (k,), grad (3k,), hess (3k,3k), d, phi'(d)) in key order."""
+    """Gradient and (unprojected) Hessian of phi_i(d_i(x)) for each key (Q22).  The stencil is the
+    support of the resolved sub-type at x (its nodes in role order): d_i does not depend on the
+    other nodes of the feature pair there (DESIGN.md R-DUP1).
+    Returns list of (support node ids (k,), grad (3k,), hess (3k,3k), d, phi'(d)) in key order."""
     out = [None] * len(keys)
     kt, kid = keys[:, 0], keys[:, 1:5]
     for t in (PP, PE, PT, EE):
         sel = np.nonzero(kt == t)[0]
         if len(sel) == 0:
             continue
-        k = NNODES[t]
         _, sub, loc = resolve_features(x, t, kid[sel])
         # group by (sub-type, local pattern)
         pat = np.concatenate([sub[:, None], loc], axis=1)
         upat, inv = np.unique(pat, axis=0, return_inverse=True)
         for pi, pr in enumerate(upat):
             idx = sel[inv.ravel() == pi]
-            ids = kid[idx, :k]
+            st, lc = int(pr[0]), pr[1:]
+            sup = lc[lc >= 0]
+            k = len(sup)
+            ids = kid[idx][:, sup]
             xs = x[ids].reshape(len(idx), 3 * k)
             V = D2.variables(xs)
-            nodes = [V[3 * j:3 * j + 3] for j in range(k)]
-            st, lc = int(pr[0]), pr[1:]
-            role = [nodes[j] for j in lc if j >= 0]
+            role = [V[3 * j:3 * j + 3] for j in range(k)]
             D = _sqdist_ad(st, role)
             d = D.sqrt()
             phi = _phi_ad(d, inA[idx], inAp[idx], mu[idx], s[idx], sigma, dhat)

@@ -101,6 +101,7 @@ _sig = {
     "bal_bench_spmv": (C.c_int, [C.c_void_p, C.c_int32, c_double_p]),
     "bal_get_trace": (C.c_int32, [C.c_void_p, c_double_p, C.c_int32]),
     "bal_spmv_counters": (C.c_int, [C.c_void_p, c_double_p]),
+    "bal_pcg_history": (C.c_int32, [C.c_void_p, c_double_p, C.c_int32]),
     "bal_kernel_launches": (C.c_int64, [C.c_void_p]),
     "bal_last_error": (C.c_char_p, [C.c_void_p]),
     "bal_destroy": (None, [C.c_void_p]),

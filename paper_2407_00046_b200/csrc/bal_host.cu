@@ -311,7 +311,7 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->xt.reserve(3 * (size_t)N);
   for (auto* b : {&c->pr, &c->pz, &c->pp, &c->pq, &c->px, &c->tmp_a, &c->tmp_b}) b->reserve(3 * (size_t)N);
   c->partials.reserve((size_t)kRedBlocks * kMaxGroups * 4 + 16 * kSMs * 4);
-  c->red.reserve(64);
+  c->red.reserve(kRedBlocks + 16);  // [0, kRedBlocks) partials, then scalar outputs
   c->counter.reserve(1);
   CK(cudaMemsetAsync(c->counter.ptr, 0, sizeof(unsigned), st));
   c->scal.reserve(1);
@@ -549,6 +549,14 @@ bal_status bal_bench_spmv(bal_ctx* c, int32_t iters, double* mean_us) {
 }
 
 int64_t bal_kernel_launches(const bal_ctx* c) { return c ? c->launches : 0; }
+
+int32_t bal_pcg_history(bal_ctx* c, double* out, int32_t max_n) {
+  if (!c || !out || max_n <= 0) return BAL_E_INVALID_ARG;
+  const int n = std::min(max_n, c->h_scal ? c->h_scal->k + 1 : 0);
+  if (n <= 0) return 0;
+  if (cudaMemcpy(out, c->hist.ptr, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return BAL_E_CUDA;
+  return n;
+}
 
 bal_status bal_spmv_counters(const bal_ctx* c, double* out) {
   if (!c || !out) return BAL_E_INVALID_ARG;

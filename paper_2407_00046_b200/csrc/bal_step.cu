@@ -267,14 +267,14 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
 }
 
 double norm2(bal_ctx* c, const double* v, int n) {
-  launch_dot(c->st, n, v, v, c->red.ptr, c->red.ptr + 1);
+  launch_dot(c->st, n, v, v, c->red.ptr, c->red.ptr + kRedBlocks + 1);
   c->launches += 2;
-  return host_scalar(c, c->red.ptr + 1);
+  return host_scalar(c, c->red.ptr + kRedBlocks + 1);
 }
 double dotp(bal_ctx* c, const double* a, const double* b, int n) {
-  launch_dot(c->st, n, a, b, c->red.ptr, c->red.ptr + 2);
+  launch_dot(c->st, n, a, b, c->red.ptr, c->red.ptr + kRedBlocks + 2);
   c->launches += 2;
-  return host_scalar(c, c->red.ptr + 2);
+  return host_scalar(c, c->red.ptr + kRedBlocks + 2);
 }
 
 void proximity(bal_ctx* c, StepWork& w, const double* x) {
@@ -287,8 +287,8 @@ void proximity(bal_ctx* c, StepWork& w, const double* x) {
 double min_d(bal_ctx* c, StepWork& w, const ConstraintSet& cs) {
   if (cs.n == 0) return INFINITY;
   w.cw.part.reserve(kRedBlocks);
-  launch_min(c->st, cs.n, cs.d.ptr, w.cw.part.ptr, c->red.ptr + 3);
-  return host_scalar(c, c->red.ptr + 3);
+  launch_min(c->st, cs.n, cs.d.ptr, w.cw.part.ptr, c->red.ptr + kRedBlocks + 3);
+  return host_scalar(c, c->red.ptr + kRedBlocks + 3);
 }
 
 // sigma0 = max(-(g_b . g_E)/||g_b||^2, mean free mass / h^2)  (Q7)
@@ -399,6 +399,14 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
   bal_step_stats S;
   std::memset(&S, 0, sizeof(S));
   c->trace.clear();
+  static const bool verbose = getenv("BAL_VERBOSE") != nullptr;
+  auto t_mark = clk::now();
+  auto mark = [&](const char* what, long long a = -1, long long b = -1) {
+    if (!verbose) return;
+    CK(cudaStreamSynchronize(st));
+    fprintf(stderr, "[bal]   %-12s %9.2f ms  %lld %lld\n", what, ms_since(t_mark), a, b);
+    t_mark = clk::now();
+  };
   for (auto* b : {&w.x, &w.xn, &w.dir, &w.rhs, &w.trial, &w.v}) b->reserve(n3);
   CK(cudaMemcpyAsync(c->xt.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   k_predictor<<<ceil_div(N, 256), 256, 0, st>>>(N, x_t, v_t, h, P.gravity[0], P.gravity[1], P.gravity[2],
@@ -406,13 +414,16 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
   CK(cudaMemcpyAsync(w.x.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   w.n_ap = 0;
   c->n_fric = 0;
+  mark("setup");
   auto t0 = clk::now();
   proximity(c, w, w.x.ptr);
+  mark("proximity", w.cand_prox.npt + w.cand_prox.nee, w.cs_A.n);
   double dmin = min_d(c, w, w.cs_A);
   S.ms_collision += ms_since(t0);
   if (!(dmin > 0.0)) throw StepFail(BAL_E_INFEASIBLE, "bal_step: input has a surface distance <= 0");
   t0 = clk::now();
   const double sig0 = sigma0(c, w, w.x.ptr);
+  mark("sigma0");
   S.ms_assembly += ms_since(t0);
   double sigma = sig0;
   double dmin_prev = INFINITY;
@@ -456,7 +467,9 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
                                                            c->fr_gam.ptr, c->fr_nrm.ptr, c->fr_lam.ptr);
       c->n_fric = nc;
     }
+    mark("union+fric", c->cset.n, c->n_fric);
     run_assembly(c, w.x.ptr, c->y.ptr, sigma);
+    mark("assembly", c->cw.nslots);
     const double en = std::sqrt(norm2(c, c->grad.ptr, 3 * N));
     S.ms_assembly += ms_since(t0);
     if (e0 < 0) e0 = en;
@@ -473,6 +486,7 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
               P.ws_max_iters, &ps);
     CK(cudaStreamSynchronize(st));
     S.ms_pcg += ms_since(t0);
+    mark("pcg", ps.ws_iters_max, c->h_scal->k);
     S.ws_iters += ps.ws_iters_max;
     int resumes = 0, halvings = 0, safeguard = 0;
     double alpha = 0.0, a_ccd = 1.0;
@@ -486,7 +500,9 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
       launch_axpy(st, 3 * N, 1.0, w.dir.ptr, w.x.ptr, w.trial.ptr);
       broad_phase(st, w.cw, w.cand_sw, c->V, c->sverts.ptr, c->F, c->tris.ptr, c->E, c->edges.ptr, w.x.ptr,
                   w.trial.ptr, dhat, c->fixed.ptr);
+      mark("swept-bp", w.cand_sw.npt, w.cand_sw.nee);
       a_ccd = ccd_step_toi(st, w.cw, w.cand_sw, w.x.ptr, w.dir.ptr, dhat);
+      mark("ccd");
       alpha = std::min(1.0, a_ccd);
       const Energy E0 = energy(c, w, w.x.ptr, w.cand_sw, sigma);
       halvings = 0;
@@ -495,6 +511,7 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
       while (alpha >= P.alpha_min) {
         launch_axpy(st, 3 * N, alpha, w.dir.ptr, w.x.ptr, w.trial.ptr);
         E1 = energy(c, w, w.trial.ptr, w.cand_sw, sigma);
+        mark("energy", E1.count);
         if (E1.count <= P.max_constraints && E1.L <= E0.L + kLsRound * std::max(E0.S, E1.S)) {
           ok = true;
           break;
@@ -524,6 +541,13 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
                                           a_ccd, alpha, (double)halvings, (double)resumes, (double)safeguard,
                                           en / e0};
     c->trace.insert(c->trace.end(), rec, rec + BAL_TRACE_FIELDS);
+    if (verbose)
+      fprintf(stderr,
+              "[bal] l=%d |A|=%d |A'|=%d dmin=%.3e sigma=%.3e ws=%d pcg=%d stop=%d a_ccd=%.3e a=%.3e halv=%d res=%d "
+              "rel_e=%.3e cand=%d/%d t=%.1fms (coll %.1f asm %.1f pcg %.1f ls %.1f)\n",
+              l, w.cs_A.n, w.n_ap, dmin, sigma, ps.ws_iters_max, c->h_scal->k, c->h_scal->stop, a_ccd, alpha, halvings,
+              resumes, en / e0, w.cand_sw.npt, w.cand_sw.nee, ms_since(t_start), S.ms_collision, S.ms_assembly,
+              S.ms_pcg, S.ms_linesearch);
     // x^{l+1} is in w.trial; its constraint set is w.cs_trial
     if (en <= P.newton_rel_tol * e0) {
       std::swap(w.x.ptr, w.trial.ptr);

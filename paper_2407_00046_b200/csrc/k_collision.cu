@@ -34,12 +34,15 @@ __global__ void k_resolve_candidates(int n, int ftype, const int4* __restrict__ 
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int4 p = pairs[i];
-  const int g[4] = {p.x, p.y, p.z, p.w};
   const Resolved r = resolve(ftype, ld3(x, p.x), ld3(x, p.y), ld3(x, p.z), ld3(x, p.w));
   if (!(r.D < dhat2)) return;
-  int gg[4];
-  for (int a = 0; a < 4; ++a) gg[a] = r.loc[a] >= 0 ? g[r.loc[a]] : -1;
-  const Key k = make_key(r.type, gg);
+  // DESIGN.md R-DUP1: the constraint is the feature pair itself (key = PT|EE + role-ordered ids)
+  Key k;
+  k.t = ftype;
+  k.n[0] = p.x;
+  k.n[1] = p.y;
+  k.n[2] = p.z;
+  k.n[3] = p.w;
   const int s = atomicAdd(count, 1);
   if (s < cap) {
     hi[s] = key_hi(k);

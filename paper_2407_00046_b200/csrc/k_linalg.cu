@@ -183,12 +183,12 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
     sc->done = 1;
     return;
   }
+  // R-PCG1: stagnation = the CG objective (monotone in PCG) decreased by no more than kStallRel of
+  // its total decrease over the last W iterations
   const int W = sc->window;
   if (W > 0 && k >= W) {
-    double older = sc->min_old;  // min over hist[0 .. k-W]
-    double recent = hist[k];
-    for (int j = k - W + 1; j < k; ++j) recent = fmin(recent, hist[j]);
-    if (recent >= older) {
+    const double* dh = hist + sc->hcap;
+    if (dh[k] - dh[k - W] <= kStallRel * dh[k]) {
       sc->stop = 1;
       sc->done = 1;
       return;
@@ -232,8 +232,9 @@ k_pcg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, 
     sc->k = 0;
     sc->stop = -1;
     sc->done = 0;
-    sc->min_old = INFINITY;
+    sc->dec = 0.0;
     hist[0] = sqrt(tot[1]);
+    hist[sc->hcap] = 0.0;
     pcg_stop_check(sc, hist);
   }
 }
@@ -268,13 +269,14 @@ k_pcg_update(int n, const double* __restrict__ dinv, const double* __restrict__ 
   }
   double tot[2];
   if (last_block_reduce<2, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
-    sc->beta = tot[0] / sc->rz;
+    sc->dec += 0.5 * alpha * sc->rz;  // phi(x + alpha p) = phi(x) - alpha rho / 2
+    sc->beta = (sc->rz != 0.0) ? tot[0] / sc->rz : 0.0;
     sc->rz = tot[0];
     sc->rr = tot[1];
     const int k = sc->k + 1;
     sc->k = k;
     hist[k] = sqrt(tot[1]);
-    if (sc->window > 0 && k - sc->window >= 0) sc->min_old = fmin(sc->min_old, hist[k - sc->window]);
+    hist[sc->hcap + k] = sc->dec;
     pcg_stop_check(sc, hist);
   }
 }

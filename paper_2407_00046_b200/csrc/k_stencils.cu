@@ -368,15 +368,26 @@ k_contact(int n, const double* __restrict__ x, const int* __restrict__ keys /*[n
   const int stride = blockDim.x;
   const int* kk = keys + 5 * (size_t)i;
   const int t = kk[0];
-  const int k = type_nodes(t);
-  d3 P[4];
-  int nd[4];
+  const int kf = type_nodes(t);
+  d3 Pf[4];
+  int ndf[4];
   for (int a = 0; a < 4; ++a) {
-    nd[a] = (a < k) ? kk[1 + a] : -1;
-    P[a] = (a < k) ? ld3(x, nd[a]) : mk(0, 0, 0);
-    nodes[4 * (size_t)i + a] = nd[a];
+    ndf[a] = (a < kf) ? kk[1 + a] : -1;
+    Pf[a] = (a < kf) ? ld3(x, ndf[a]) : mk(0, 0, 0);
   }
-  const Resolved rs = resolve(t, P[0], P[1], P[2], P[3]);
+  const Resolved rf = resolve(t, Pf[0], Pf[1], Pf[2], Pf[3]);
+  // stencil = support of the resolved sub-type, in role order (DESIGN.md R-DUP1)
+  const int k = type_nodes(rf.type);
+  d3 P[4];
+  Resolved rs;
+  rs.type = rf.type;
+  rs.D = rf.D;
+  for (int a = 0; a < 4; ++a) {
+    const int src = (a < k) ? rf.loc[a] : -1;
+    P[a] = src >= 0 ? Pf[src] : mk(0, 0, 0);
+    rs.loc[a] = (a < k) ? a : -1;
+    nodes[4 * (size_t)i + a] = src >= 0 ? ndf[src] : -1;
+  }
   const double D = rs.D, d = sqrt(D);
   double p1, p2;
   phi_derivs(d, inA[i], inAp[i], mu[i], s[i], sigma, dhat, p1, p2);

@@ -35,9 +35,10 @@ struct Bsr {
 
 // PCG scalars living in device memory (single group)
 struct PcgScal {
-  double rz, pq, alpha, beta, rr, bnorm, tol, min_old;
-  int k, stop, done, max_iters, window, pad;
+  double rz, pq, alpha, beta, rr, bnorm, tol, dec;
+  int k, stop, done, max_iters, window, hcap;  // hist[0..hcap) = ||r_k||, hist[hcap..) = phi_0 - phi_k
 };
+constexpr double kStallRel = 1e-10;  // DESIGN.md R-PCG1
 // warm-start per-group scalars
 struct GrpScal {
   double rz[kMaxGroups], pq[kMaxGroups], alpha[kMaxGroups], beta[kMaxGroups], rr[kMaxGroups],

@@ -87,6 +87,10 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
       c->spmv_bytes_moved += c->spmv_moved_bytes();
     }
     if (c->h_scal->done) break;
+    static const bool verbose = getenv("BAL_VERBOSE_PCG") != nullptr;
+    if (verbose && (c->h_scal->k % 512) < kBatch)
+      fprintf(stderr, "[bal-pcg] k=%d rr=%.3e bnorm=%.3e alpha=%.3e beta=%.3e\n", c->h_scal->k,
+              std::sqrt(c->h_scal->rr), c->h_scal->bnorm, c->h_scal->alpha, c->h_scal->beta);
   }
   if (stats) {
     double rn = 0.0;
@@ -103,7 +107,10 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   const int N = c->N;
   const Bsr S = c->static_bsr(), C = c->contact_bsr();
   if (stats) std::memset(stats, 0, sizeof(*stats));
-  if ((int)c->hist.cap < max_iters + 8) c->hist.reserve(max_iters + 8);
+  // hist[0, hcap): ||r_k||; hist[hcap, 2 hcap): cumulative CG objective decrease (R-PCG1).  Sized for
+  // App. B resumes up to the max_pcg cap as well.
+  const int hcap = std::max(max_iters, c->prm.max_pcg) + 8;
+  if (c->hist.cap < 2 * (size_t)hcap) c->hist.reserve(2 * (size_t)hcap);
   // ---------------- warm start: per-group PCG on A_GG (Q20)
   if (warm) {
     compact_groups(c);
@@ -131,6 +138,8 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
       int any = 0;
       CK(cudaMemcpyAsync(&any, &c->gscal.ptr->any_active, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      static const bool verbose = getenv("BAL_VERBOSE_PCG") != nullptr;
+      if (verbose) fprintf(stderr, "[bal-ws] it=%d G=%d any=%d\n", done_iters, c->ngroups, any);
       if (!any) break;
     }
     if (stats) {
@@ -154,6 +163,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.tol = tol;
   h.window = window;
   h.max_iters = max_iters;
+  h.hcap = hcap;
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
   launch_pcg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->partials.ptr, c->counter.ptr,

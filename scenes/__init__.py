@@ -234,11 +234,14 @@ def make_cubes(seed=1, cells=5, edge=1.0, E=1e5, nu=0.4, rho=1e3, gap=0.01, spee
 
 
 def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0):
-    """Tiny fixture: one generically rotated tet above a plane."""
+    """Tiny fixture: one generically rotated tet above a plane.  The gap is made generic
+    (height * (1 + U(0.05, 0.15))): with an exact decimal gap and a vertical approach the CCD
+    backtracking (x0.9 of the time of coplanarity, i.e. x0.1 of the gap) produces distances of
+    exactly 1e-3, 1e-4, 1e-5 = 1e-2 dhat, a tie on Alg. 1's strict 'min d < 1e-2 dhat' test."""
     rng = np.random.default_rng(seed)
     x = np.array([[0, 0, 0], [0.1, 0, 0], [0, 0.1, 0], [0, 0, 0.1]], dtype=np.float64)
     x = (x - x.mean(0)) @ random_rotation(rng).T
-    x[:, 1] += -x[:, 1].min() + height
+    x[:, 1] += -x[:, 1].min() + height * (1.0 + rng.uniform(0.05, 0.15))
     tets = _orient(x, np.array([[0, 1, 2, 3]]))
     sb = SceneBuilder()
     sb.add_body(x, tets, 0, v0=(0.0, -speed, 0.0))
@@ -328,8 +331,9 @@ def spiky_ball_occ(R, n_spikes, spike_len, spike_r=0.75):
     return occ, ext
 
 
-def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=19.6, n_spikes=110,
-                    spike_len=15.0, n_balls=4, E_ball=5e5, E_net=1e9, nu=0.4, rho=1e3, chi=0.3, drop_gap=0.002):
+def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=20.4, n_spikes=110,
+                    spike_len=15.0, n_balls=4, E_ball=5e5, E_net=1e9, nu=0.4, rho=1e3, chi=0.3, drop_gap=0.002,
+                    jitter_deg=(0.2, 0.8)):
     """C4 recipe (Table 1 row 1 P:664 for the statistics): a chain-net of
     interlocked 1-voxel-thick square rings (horizontal rings on an nx x nz lattice plus vertical
     connector rings threading neighbours through their holes; outermost horizontal rings fixed)
@@ -338,17 +342,20 @@ def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=19
     Defaults target T ~ 1.76M tets, N ~ 0.8M nodes."""
     rng = np.random.default_rng(seed)
     sb = SceneBuilder()
+    assert L == 8 and spacing == 10, "connector layout below is laid out for L=8, spacing=10"
     xr, tr = voxel_mesh(_ring_xz(L), voxel)
-    cx_occ = _ring_xy(spacing - L + L // 2 * 2 - 1 + 2, 9)
-    # connector between horizontal rings along x: vertical beams inside both holes
-    conn_len = spacing - 1  # x span in voxels
+    # Hole of every horizontal ring: [1,7)^2 (voxels, ring-local).  Vertical beams threading it:
+    #   x-connector (xy plane, z in [4.5,5.5)): own near beam x in [4.5,5.5), incoming far beam [1.5,2.5)
+    #   z-connector (zy plane, x in [3,4)):     own near beam z in [4.5,5.5), incoming far beam [1.5,2.5)
+    # -> every pair of distinct rings is >= 0.5 voxel apart before the jitter rotations.
+    conn_len = 8
     xcx, tcx = voxel_mesh(_ring_xy(conn_len, 9), voxel)
     xcz, tcz = voxel_mesh(_ring_zy(conn_len, 9), voxel)
 
     def jitter(x):
         c = x.mean(0)
         ax = rng.normal(size=3)
-        R = rot_axis(ax, np.deg2rad(rng.uniform(0.2, 0.8)))
+        R = rot_axis(ax, np.deg2rad(rng.uniform(*jitter_deg)))
         return (x - c) @ R.T + c
 
     for i in range(nx):
@@ -361,12 +368,11 @@ def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=19
             sb.add_body(x, tr, 1, fixed=np.full(len(xr), 1 if border else 0, np.uint8))
             if i + 1 < nx:
                 # vertical ring in the xy plane through the holes of rings (i,k) and (i+1,k)
-                oc = o + np.array([L // 2 + 1, -4, L // 2 - 0.5]) * voxel
+                oc = o + np.array([4.5, -4.0, 4.5]) * voxel
                 sb.add_body(jitter(xcx + oc), tcx, 1)
             if k + 1 < nz:
-                oc = o + np.array([L // 2 - 0.5, -4, L // 2 + 1]) * voxel
+                oc = o + np.array([3.0, -4.0, 4.5]) * voxel
                 sb.add_body(jitter(xcz + oc), tcz, 1)
-    del cx_occ
     occ, ext = spiky_ball_occ(ball_R, n_spikes, spike_len)
     xb, tb = voxel_mesh(occ, voxel)
     xb = xb - ext * voxel

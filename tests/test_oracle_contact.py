@@ -65,14 +65,27 @@ def test_axis_aligned_cases():
     assert t[0] == cm.EE and D[0] == pytest.approx(4.0, rel=1e-14)
 
 
-def test_dedup_point_near_shared_edge():
-    """Q28: a PE reached from the two triangles sharing the edge (and from EE pairs) counts once."""
+def test_feature_pairs_are_constraints_and_barrier_is_continuous():
+    """R-DUP1: each vertex-triangle / edge-edge pair is its own constraint with its own feature
+    distance, so the barrier sum is continuous when a vertex slides across a shared edge (merging
+    the two point-edge duplicates, makes it jump by ~b(d))."""
+    dhat = 1e-3
     x = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.5, 1.0, -1.0], [0.5, -1.0, -1.0], [0.5, 0.0001, 0.0005]])
     # roof: triangles (0,1,2) and (0,3,1) share the ridge edge (0,1); point 4 hovers over the ridge
     pt = np.array([[4, 0, 1, 2], [4, 0, 3, 1]])
-    keys, d = cm.constraint_set(x, pt, np.zeros((0, 4), np.int64), 1e-3)
-    assert len(keys) == 1 and keys[0, 0] == cm.PE and list(keys[0, 1:4]) == [4, 0, 1]
-    assert d[0] == pytest.approx(np.hypot(0.0001, 0.0005), rel=1e-12)
+    keys, d = cm.constraint_set(x, pt, np.zeros((0, 4), np.int64), dhat)
+    assert len(keys) == 2 and set(keys[:, 0]) == {cm.PT}
+    np.testing.assert_allclose(d, np.hypot(0.0001, 0.0005), rtol=1e-12)
+    # slide the vertex across the ridge at constant height above the roof: the sum stays smooth
+    ys = np.linspace(-4e-4, 4e-4, 801)
+    tot = []
+    for yy in ys:
+        xx = x.copy()
+        xx[4] = [0.5, yy, 0.0005 - abs(yy)]
+        k, dd = cm.constraint_set(xx, pt, np.zeros((0, 4), np.int64), dhat)
+        tot.append(np.sum(barrier(dd, dhat)))
+    jumps = np.abs(np.diff(tot))
+    assert jumps.max() <= 0.02 * max(tot)
 
 
 def test_contact_stencil_derivatives_fd():

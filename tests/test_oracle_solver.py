@@ -64,8 +64,7 @@ def _dense_brute(o, x, asm):
         for a, n in enumerate(tet):
             S[3 * a:3 * a + 3, 3 * n:3 * n + 3] = np.eye(3)
         A += S.T @ asm["elastic_P"][e] @ S
-    for key, P in zip(asm["contact_keys"], asm["contact_P"]):
-        ids = [i for i in key[1:] if i >= 0]
+    for ids, P in zip(asm["contact_ids"], asm["contact_P"]):
         S = np.zeros((3 * len(ids), 3 * N))
         for a, n in enumerate(ids):
             S[3 * a:3 * a + 3, 3 * n:3 * n + 3] = np.eye(3)
@@ -159,6 +158,7 @@ def test_pcg_special_cases_and_dense_solve():
     assert np.linalg.norm(st.x - xd) <= 1e-9 * np.linalg.norm(xd)
     # App. B stagnation: a stalled residual history stops the solve
     s2 = la.PCGState(np.zeros(3), np.ones(3), np.ones(3), np.ones(3), 1.0, [1.0] * 101, 1.0)
+    s2.dec = [1.0] * 101  # CG objective did not decrease over the last 100 iterations (R-PCG1)
     la.pcg_run(sp.identity(3, format="csr"), np.tile(np.eye(3), (1, 1, 1)), s2, 1e-4, 100, 10 ** 6)
     assert s2.stop == la.STOP_STAGNATED
 
