@@ -95,6 +95,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def job_throughput(local_seconds, units_per_rank, world, device):
+    """Max of the ranks' timed-region seconds (the job time) and the whole-job throughput
+    (units processed by all ranks / job time).  One all_reduce(MAX) when world > 1."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(local_seconds)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    s = float(t.item())
+    return s, world * units_per_rank / s
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -238,12 +250,9 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     launches = ctx.kernel_launches - launches0
     spmv1 = bal.bal_spmv_counters(ctx)
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    s_frame = ms_max / 1000.0 / args.steps
-    fps = world * args.steps / (ms_max / 1000.0)
+    s_max, fps = job_throughput(ms / 1000.0, args.steps, world, dev)
+    ms_max = 1000.0 * s_max
+    s_frame = s_max / args.steps
     pcg = sum(s["pcg_iters"] for s in stats)
     pcg_ms = sum(s["ms_pcg"] for s in stats)
     newton = sum(s["newton_iters"] for s in stats)
@@ -274,12 +283,9 @@ def run_ours(args):
         for _ in range(ne):
             xh, vh, _s = bal.bal_step_host(ctx, xh, vh)
         el = time.perf_counter() - t0
-        te = torch.tensor([el], device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        _s, e2e_fps = job_throughput(el, ne, world, dev)
         nb = 2 * 3 * 8 * len(sc["rest_x"])
-        e2e = {"value": world * ne / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": nb,
-               "d2h_bytes_per_step": nb}
+        e2e = {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -317,7 +317,7 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->scal.reserve(1);
   c->gscal.reserve(1);
   c->hist.reserve(std::max(c->prm.max_pcg, 1) + 8);
-  CK(cudaMallocHost(&c->h_scal, sizeof(PcgScal)));
+  CK(cudaMallocHost(&c->h_scal, 3 * sizeof(PcgScal)));  // [0] current, [1..2] graph ping-pong copies
   CK(cudaStreamSynchronize(st));
 }
 
@@ -573,8 +573,12 @@ void bal_destroy(bal_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   destroy_step_work(c);
+  if (c->ev_ready)
+    for (cudaEvent_t e : c->ev)
+      if (e) cudaEventDestroy(e);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
 

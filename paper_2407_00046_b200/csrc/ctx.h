@@ -11,6 +11,7 @@
 struct bal_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // CUDA-graph capture only (pcg.cu)
   cudaStream_t st = nullptr;
   bal_params prm{};
   int N = 0, T = 0;
@@ -62,7 +63,7 @@ struct bal_ctx {
   bal::DevBuf<int> tmp_i;
 
   // ---- SpMV instrumentation (CUDA events around every PCG SpMV launch)
-  cudaEvent_t ev[16] = {};
+  cudaEvent_t ev[2 * (2 * 8 + 1)] = {};  // two ping-pong sets of (2 kBatch + 1) events (pcg.cu)
   bool ev_ready = false;
   double spmv_ms = 0.0, spmv_bytes_alg = 0.0, spmv_bytes_moved = 0.0;
   long long spmv_count = 0;

@@ -28,24 +28,40 @@ BAL_D void row_accum(const Bsr& A, int row, int lane, const double* __restrict__
                      int gr, double& a0, double& a1, double& a2) {
   const int beg = __ldg(A.row_ptr + row), end = __ldg(A.row_ptr + row + 1);
   const double* __restrict__ vals = A.val + 9 * (size_t)beg;
-  const int nf = 9 * (end - beg);
-  int f = lane;
-  int blk = f / 9;
-  int rem = f - 9 * blk;
-  for (; f < nf; f += kSL) {
-    const int col = __ldg(A.col + beg + blk);
-    const double a = __ldcs(vals + f);  // streamed once per SpMV: evict-first
-    const int r = rem / 3, c = rem - 3 * r;
-    double pr = a * __ldg(v + 3 * (size_t)col + c);
-    if (MASK && __ldg(grp + col) != gr) pr = 0.0;
-    if (r == 0) a0 += pr;
-    else if (r == 1) a1 += pr;
-    else a2 += pr;
-    rem += kSL % 9;
-    blk += kSL / 9;
-    if (rem >= 9) {
-      rem -= 9;
-      ++blk;
+  const int* __restrict__ cols = A.col + beg;
+  const unsigned nf = 9u * (unsigned)(end - beg);
+  // kU independent element loads in flight per lane (memory-level parallelism): the row's values
+  // are contiguous, so each unrolled load is a fully coalesced 128 B access of the sub-warp
+  constexpr int kU = 4;
+  for (unsigned f0 = lane; f0 < nf; f0 += kU * kSL) {
+    double a[kU], xv[kU];
+    unsigned rr[kU];
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const unsigned f = f0 + j * kSL;
+      a[j] = 0.0;
+      rr[j] = 0;
+      if (f < nf) a[j] = __ldcs(vals + f);  // streamed once per SpMV: evict-first
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const unsigned f = f0 + j * kSL;
+      xv[j] = 0.0;
+      if (f < nf) {
+        const unsigned blk = f / 9u, rem = f - 9u * blk;
+        const unsigned r = rem / 3u, c = rem - 3u * r;
+        const int col = __ldg(cols + blk);
+        xv[j] = __ldg(v + 3 * (size_t)col + c);
+        if (MASK && __ldg(grp + col) != gr) xv[j] = 0.0;
+        rr[j] = r;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const double pr = a[j] * xv[j];
+      if (rr[j] == 0) a0 += pr;
+      else if (rr[j] == 1) a1 += pr;
+      else a2 += pr;
     }
   }
 }

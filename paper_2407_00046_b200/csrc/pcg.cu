@@ -54,44 +54,78 @@ void compact_groups(bal_ctx* c) {
   c->launches += 2;
 }
 
+// One batch = kBatch PCG iterations (SpMV+dot, update, p-update) + a D2H copy of the scalars and a
+// completion event, captured once per solve into a CUDA graph.  Two graphs (ping-pong event sets
+// and host buffers) keep one batch queued while the host inspects the previous one, so the GPU never
+// idles on the host; kernels early-exit once the device `done` flag is set.
+static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaGraphExec_t* out) {
+  // capture on a private stream (the user's stream may be the legacy default stream, which cannot be
+  // captured); the instantiated graph is then launched on the user's stream
+  if (!c->cap_stream) CK(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t st = c->cap_stream;
+  const int N = c->N;
+  cudaEvent_t* ev = c->ev + set * (2 * kBatch + 1);
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int it = 0; it < kBatch; ++it) {
+    // CUDA events bracket every SpMV launch: the bench reports the SpMV kernel's average duration
+    // inside the timed region from these (roofline achieved GB/s)
+    CK(cudaEventRecord(ev[2 * it], st));
+    launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
+    CK(cudaEventRecord(ev[2 * it + 1], st));
+    launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
+                      c->counter.ptr, c->scal.ptr, c->hist.ptr);
+    launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
+  }
+  CK(cudaMemcpyAsync(c->h_scal + 1 + set, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ev[2 * kBatch], st));
+  CK(cudaStreamEndCapture(st, &g));
+  CK(cudaGraphInstantiate(out, g, 0));
+  CK(cudaGraphDestroy(g));
+}
+
 static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* stats) {
   cudaStream_t st = c->st;
-  const int N = c->N;
   if (!c->ev_ready) {
-    for (int i = 0; i < 2 * kBatch; ++i) CK(cudaEventCreate(&c->ev[i]));
+    for (int i = 0; i < 2 * (2 * kBatch + 1); ++i) CK(cudaEventCreate(&c->ev[i]));
     c->ev_ready = true;
   }
+  cudaGraphExec_t ge[2];
+  capture_batch(c, S, C, 0, &ge[0]);
+  capture_batch(c, S, C, 1, &ge[1]);
+  int k_prev = c->h_scal->k;
+  CK(cudaGraphLaunch(ge[0], st));
+  CK(cudaGraphLaunch(ge[1], st));
+  c->launches += 6 * kBatch;
+  int cur = 0;
   while (true) {
-    const int k0 = c->h_scal->k;
-    for (int it = 0; it < kBatch; ++it) {
-      // CUDA events bracket every SpMV launch: the bench reports the SpMV kernel's average
-      // duration inside the timed region from these (roofline achieved GB/s)
-      CK(cudaEventRecord(c->ev[2 * it], st));
-      launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
-      CK(cudaEventRecord(c->ev[2 * it + 1], st));
-      launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
-                        c->counter.ptr, c->scal.ptr, c->hist.ptr);
-      launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
-      c->launches += 3;
-    }
-    CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    // only launches that did work (iterations k0 .. k-1) count towards the SpMV timing
-    const int worked = std::min(kBatch, c->h_scal->k - k0);
+    cudaEvent_t* ev = c->ev + cur * (2 * kBatch + 1);
+    CK(cudaEventSynchronize(ev[2 * kBatch]));
+    const PcgScal hs = c->h_scal[1 + cur];
+    // only launches that did work (iterations k_prev .. k-1) count towards the SpMV timing
+    const int worked = std::min(kBatch, hs.k - k_prev);
     for (int it = 0; it < worked; ++it) {
       float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, c->ev[2 * it], c->ev[2 * it + 1]));
+      CK(cudaEventElapsedTime(&ms, ev[2 * it], ev[2 * it + 1]));
       c->spmv_ms += ms;
       c->spmv_count += 1;
       c->spmv_bytes_alg += c->spmv_alg_bytes();
       c->spmv_bytes_moved += c->spmv_moved_bytes();
     }
-    if (c->h_scal->done) break;
+    k_prev = hs.k;
+    if (hs.done) break;
     static const bool verbose = getenv("BAL_VERBOSE_PCG") != nullptr;
-    if (verbose && (c->h_scal->k % 512) < kBatch)
-      fprintf(stderr, "[bal-pcg] k=%d rr=%.3e bnorm=%.3e alpha=%.3e beta=%.3e\n", c->h_scal->k,
-              std::sqrt(c->h_scal->rr), c->h_scal->bnorm, c->h_scal->alpha, c->h_scal->beta);
+    if (verbose && (hs.k % 512) < kBatch)
+      fprintf(stderr, "[bal-pcg] k=%d rr=%.3e bnorm=%.3e alpha=%.3e beta=%.3e\n", hs.k, std::sqrt(hs.rr), hs.bnorm,
+              hs.alpha, hs.beta);
+    CK(cudaGraphLaunch(ge[cur], st));  // re-queue this set behind the other in-flight batch
+    c->launches += 3 * kBatch;
+    cur ^= 1;
   }
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGraphExecDestroy(ge[0]));
+  CK(cudaGraphExecDestroy(ge[1]));
+  CK(cudaMemcpy(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost));
   if (stats) {
     double rn = 0.0;
     CK(cudaMemcpy(&rn, c->hist.ptr + c->h_scal->k, sizeof(double), cudaMemcpyDeviceToHost));

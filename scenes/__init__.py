@@ -233,7 +233,7 @@ def make_cubes(seed=1, cells=5, edge=1.0, E=1e5, nu=0.4, rho=1e3, gap=0.01, spee
     return sb.build([(E, nu, rho)], "C1-cubes", chi=0.0)
 
 
-def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0):
+def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0, vt=0.0, chi=0.0):
     """Tiny fixture: one generically rotated tet above a plane.  The gap is made generic
     (height * (1 + U(0.05, 0.15))): with an exact decimal gap and a vertical approach the CCD
     backtracking (x0.9 of the time of coplanarity, i.e. x0.1 of the gap) produces distances of
@@ -244,10 +244,10 @@ def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0):
     x[:, 1] += -x[:, 1].min() + height * (1.0 + rng.uniform(0.05, 0.15))
     tets = _orient(x, np.array([[0, 1, 2, 3]]))
     sb = SceneBuilder()
-    sb.add_body(x, tets, 0, v0=(0.0, -speed, 0.0))
+    sb.add_body(x, tets, 0, v0=(vt, -speed, 0.0))
     px, pt = _plane(1.0)
     sb.add_obstacle(px, pt)
-    return sb.build([(E, nu, rho)], "tet")
+    return sb.build([(E, nu, rho)], "tet", chi=chi)
 
 
 def perturbed(scene, seed, scale):

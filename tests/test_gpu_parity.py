@@ -228,3 +228,33 @@ def test_bad_mesh_and_args_fail_loudly():
     with pytest.raises(bal.BalError) as ei:
         bal.bal_init(bad)
     assert ei.value.status == -2
+
+
+# --------------------------------------------------------------------------- friction (a5)
+def test_friction_stencils_and_assembly_parity(cubes_state):
+    sc, o, x1, v1 = cubes_state
+    sc = dict(sc)
+    sc["params"] = dict(sc["params"], chi=0.5)
+    o = Oracle(sc)
+    x = x1
+    pt, ee = cm.candidates(o.mesh, x, x, o.dhat)
+    keys, d = cm.constraint_set(x, pt, ee, o.dhat)
+    sigma = 3.7e5
+    y = sc["x0"] + o.h * sc["v0"] + o.h ** 2 * o.g[None]
+    x_t = x - 0.004 * np.random.default_rng(3).normal(size=x.shape) * (~o.mesh.fixed[:, None])
+    st = oracle_state(o, x, y=y, sigma=sigma)
+    st["x_t"] = x_t
+    fk, G, n, lam = o.friction_anchors(x, st, keys)
+    st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"] = fk, G, n, lam
+    asm = o.assemble(x, st, keys)
+    ctx = bal.bal_init(sc)
+    out = bal.bal_assemble(ctx, _t(x), active_keys=keys, sigma=sigma, y=y, x_t=x_t,
+                           friction=dict(keys=fk, gamma=G, n=n, lam=lam))
+    N = o.N
+    Ag = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
+    Ag = Ag + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
+    Ao = asm["A"]
+    rowscale = np.asarray(abs(Ao).sum(axis=1)).ravel() + 1e-300
+    assert (np.asarray(abs(Ag - Ao).sum(axis=1)).ravel() / rowscale).max() <= 1e-9
+    ge = _np(out["grad"])
+    assert np.linalg.norm(ge - asm["grad"]) <= 1e-9 * np.linalg.norm(asm["grad"])
