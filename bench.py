@@ -2,11 +2,16 @@
 """Benchmark of the BAL inexact Newton-PCG time step (arXiv 2407.00046) on B200.
 
 Metric (BASELINE.json): "seconds/frame & PCG iters/s at 1.76M tets; BSR SpMV HBM GB/s vs peak".
-One bench step = one bal_step = one frame (h = 1/30 s) of the C4 puffer-balls-on-chain-net scene
-(configs[3], ~1.7M tets) -- every row of SURVEY §8(a): constraint sets, elastic / contact / friction
-stencils, atomic-free assembly, warm start, PCG, CCD line search, AL updates.
-`value` = frames/s of the whole job (N ranks each advance their own replica of the scene: weak
-scaling, no data-path collective).  Extra keys: seconds/frame, PCG iterations/s, SpMV roofline.
+Workload: the C4 puffer-balls-on-chain-net scene (configs[3], ~1.75M tets, dt = 1/30 s).  A C4
+frame takes hundreds of inexact-Newton iterations of thousands of PCG iterations each (the paper
+reports 156.8 Newton iterations and 427 s per frame on its GPU), so one bench step is ONE
+inexact-Newton iteration of Alg. 1 -- every row of SURVEY §8(a) once: constraint sets, elastic /
+contact / friction stencils, atomic-free assembly, warm start, global PCG, CCD line search, AL
+updates (a1 at every frame start) -- and the simulation continues across steps, frame after frame.
+`value` = global PCG iterations per second of the whole job (all phases in the denominator; N
+ranks each advance their own replica: weak scaling, no data-path collective).  Seconds per frame
+are reported when a frame completes inside the timed region, and as ms/Newton x the Newton
+iterations per frame of a recorded long run (profiles/c4_frames.json) otherwise, labelled so.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c1]
 """
@@ -26,16 +31,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "seconds/frame & PCG iters/s at 1.76M tets; BSR SpMV HBM GB/s vs peak"
-# Newton / PCG counts of the C4 frames observed on the GPU path (profiles/bench_r01.md); used only
-# to scale the reference (oracle) arm's bounded sample to a frame.
-C4_NEWTON_PER_FRAME = 40.0
-C4_PCG_PER_NEWTON = 150.0
+UNIT = "PCG iters/s"
+# PCG iterations per Newton iteration observed on the GPU path on C4 (gpurun_out probe runs, round 1);
+# used only to size the reference (oracle) arm's step.
+C4_PCG_PER_NEWTON = 6000.0
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=["c4", "c1"])
@@ -182,24 +187,73 @@ def run_reference(args):
     if rank != 0:
         return
     sc, wl = make_scene(args.config)
+    ppn = C4_PCG_PER_NEWTON if args.config == "c4" else 100.0
     vals = []
     t_all = time.perf_counter()
     info = {}
     for _ in range(max(args.warmup, 0)):
-        oracle_sample(sc, C4_NEWTON_PER_FRAME, C4_PCG_PER_NEWTON, budget_tets=2000)
+        oracle_sample(sc, 1.0, ppn, budget_tets=2000)
+    threads, desc = 0, ""
     for k in range(args.steps):
-        s_frame, threads, desc, info = oracle_sample(sc, C4_NEWTON_PER_FRAME, C4_PCG_PER_NEWTON, seed=k)
-        vals.append(s_frame)
-    s_frame = float(np.mean(vals))
-    fps = 1.0 / s_frame
-    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * s_frame, "higher_is_better": True,
+        _s, threads, desc, info = oracle_sample(sc, 1.0, ppn, budget_tets=5000, seed=k)
+        vals.append(info["t_assembly_s"] + ppn * info["t_pcg_iter_s"])
+    s_newton = float(np.mean(vals))
+    v = ppn / s_newton
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * s_newton, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"]))},
-            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": desc},
-            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+                       "step": "one inexact-Newton iteration of Alg. 1"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": desc + f"; one step = assembly + {ppn:.0f} PCG iterations (extrapolated)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "detail": {**info, "wall_s": time.perf_counter() - t_all}}
     print(json.dumps(line), flush=True)
+
+
+class FrameRunner:
+    """Advances the simulation one inexact-Newton iteration (= one bench step: every §8(a) row
+    a2-a11 once; a1 at each frame start) at a time through bal_frame_begin/iterate/finish,
+    starting the next frame whenever one converges.  Keeps running totals of the library's
+    per-frame counters."""
+
+    def __init__(self, bal, ctx, x, v):
+        import torch
+        self.bal, self.ctx = bal, ctx
+        self.x, self.v = x, v
+        self.xn, self.vn = torch.empty_like(x), torch.empty_like(v)
+        self.done = {"pcg_iters": 0, "newton_iters": 0, "ws_iters": 0, "ms_collision": 0.0, "ms_assembly": 0.0,
+                     "ms_pcg": 0.0, "ms_linesearch": 0.0, "max_constraints": 0}
+        self.frames = []  # (ms_total, newton_iters, pcg_iters) of completed frames
+        self.unconverged = 0
+        bal.bal_frame_begin(ctx, self.x, self.v)
+
+    def totals(self):
+        cur = self.bal.bal_frame_stats(self.ctx)
+        t = dict(self.done)
+        for k in t:
+            if k == "max_constraints":
+                t[k] = max(t[k], cur[k])
+            else:
+                t[k] += cur[k]
+        return t
+
+    def step(self):
+        try:
+            conv = self.bal.bal_frame_iterate(self.ctx, 1)
+        except self.bal.BalError as e:  # Newton cap (BAL_E_NOT_CONVERGED): the frame ends unconverged
+            if e.status != -4:
+                raise
+            self.unconverged += 1
+            conv = True
+        if conv:
+            st = self.bal.bal_frame_finish(self.ctx, self.xn, self.vn, allow_unconverged=True)
+            for k in self.done:
+                self.done[k] = max(self.done[k], st[k]) if k == "max_constraints" else self.done[k] + st[k]
+            self.frames.append((st["ms_total"], st["newton_iters"], st["pcg_iters"]))
+            self.x, self.xn = self.xn, self.x
+            self.v, self.vn = self.vn, self.v
+            self.bal.bal_frame_begin(self.ctx, self.x, self.v)
 
 
 def run_ours(args):
@@ -217,21 +271,20 @@ def run_ours(args):
 
     sc, wl = make_scene(args.config)
     ctx = bal.bal_init(sc, device=local)
-    x = torch.as_tensor(sc["x0"].ravel(), device=dev)
-    v = torch.as_tensor(sc["v0"].ravel(), device=dev)
-    xn, vn = torch.empty_like(x), torch.empty_like(v)
     stream = torch.cuda.current_stream(dev)
     bal.bal_set_stream(ctx, stream)
+    x = torch.as_tensor(sc["x0"].ravel(), device=dev)
+    v = torch.as_tensor(sc["v0"].ravel(), device=dev)
+    run = FrameRunner(bal, ctx, x, v)
     for _ in range(args.warmup):
-        bal.bal_step(ctx, x, v, xn, vn)
-        x, xn = xn, x
-        v, vn = vn, v
+        run.step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     spmv0 = bal.bal_spmv_counters(ctx)
     launches0 = ctx.kernel_launches
-    stats = []
+    tot0 = run.totals()
+    nf0 = len(run.frames)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
@@ -240,9 +293,7 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            stats.append(bal.bal_step(ctx, x, v, xn, vn))
-            x, xn = xn, x
-            v, vn = vn, v
+            run.step()
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -250,12 +301,13 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     launches = ctx.kernel_launches - launches0
     spmv1 = bal.bal_spmv_counters(ctx)
-    s_max, fps = job_throughput(ms / 1000.0, args.steps, world, dev)
+    tot1 = run.totals()
+    d = {k: tot1[k] - tot0[k] for k in tot1 if k != "max_constraints"}
+    pcg = d["pcg_iters"]
+    newton = d["newton_iters"]
+    s_max, pcg_per_s = job_throughput(ms / 1000.0, pcg, world, dev)
     ms_max = 1000.0 * s_max
-    s_frame = s_max / args.steps
-    pcg = sum(s["pcg_iters"] for s in stats)
-    pcg_ms = sum(s["ms_pcg"] for s in stats)
-    newton = sum(s["newton_iters"] for s in stats)
+    new_frames = run.frames[nf0:]
     # SpMV roofline from the library's CUDA events around every SpMV launch in the timed region
     d_ms = spmv1["ms"] - spmv0["ms"]
     d_n = spmv1["launches"] - spmv0["launches"]
@@ -270,51 +322,80 @@ def run_ours(args):
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    # e2e through the public API with host buffers (bal_step_host: H2D + D2H inside the call)
+    # e2e through the public API with host buffers: pinned x_t, v_t -> device, the same number of
+    # Newton iterations of a frame, x back to the host, all inside the timed region
     e2e = None
     if not args.no_e2e:
-        xh = x.cpu().numpy()
-        vh = v.cpu().numpy()
-        ne = max(1, min(args.steps, 2))
+        xh = x.detach().cpu().pin_memory()
+        vh = v.detach().cpu().pin_memory()
+        xo = torch.empty_like(xh).pin_memory()
+        ne = max(1, min(args.steps, 3))
+        xd, vd, xnd = torch.empty_like(x), torch.empty_like(v), torch.empty_like(x)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        xd.copy_(xh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        bal.bal_frame_begin(ctx, xd, vd)
+        p0 = 0
+        conv = False
         for _ in range(ne):
-            xh, vh, _s = bal.bal_step_host(ctx, xh, vh)
+            conv = bal.bal_frame_iterate(ctx, 1)
+            if conv:
+                break
+        pe = bal.bal_frame_stats(ctx)["pcg_iters"] - p0
+        bal.bal_frame_finish(ctx, xnd, None, allow_unconverged=True)  # x_next = last accepted iterate
+        xo.copy_(xnd, non_blocking=True)
+        torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        _s, e2e_fps = job_throughput(el, ne, world, dev)
-        nb = 2 * 3 * 8 * len(sc["rest_x"])
-        e2e = {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
+        _s, e2e_v = job_throughput(el, pe, world, dev)
+        nb = 3 * 8 * len(sc["rest_x"])
+        e2e = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * nb / ne, "d2h_bytes_per_step": nb / ne,
+               "steps": ne, "note": "x_t, v_t H2D from pinned memory + frame setup + ne Newton iterations + x D2H"}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
+    ppn = pcg / max(newton, 1)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        npf = newton / max(args.steps, 1)
-        ppn = pcg / max(newton, 1)
-        s_or, threads, desc, _info = oracle_sample(sc, npf, ppn)
-        cpu = {"value": 1.0 / s_or, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": desc}
+        _s, threads, desc, info = oracle_sample(sc, 1.0, ppn)
+        s_newton_cpu = info["t_assembly_s"] + ppn * info["t_pcg_iter_s"]
+        cpu = {"value": ppn / s_newton_cpu, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": desc + f"; one step = assembly + {ppn:.0f} PCG iterations (the GPU run's mean), "
+                                f"extrapolated"}
+    ms_newton = ms_max / max(newton, 1)
+    npf_ref = None
+    rf = os.path.join(ROOT, "profiles", f"{args.config}_frames.json")
+    if os.path.exists(rf):
+        with open(rf) as f:
+            npf_ref = json.load(f).get("newton_per_frame")
     line = {
-        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": pcg_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+                   "step": "one inexact-Newton iteration of Alg. 1 (constraint sets, stencils, assembly, warm "
+                           "start, PCG, CCD line search, AL updates); frames continue across steps",
                    "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (system ~0.8 GB/iteration)"},
-        "seconds_per_frame": s_frame,
-        "pcg_iters_per_s": pcg / (pcg_ms / 1000.0) if pcg_ms > 0 else None,
-        "newton_iters_per_frame": newton / args.steps,
-        "pcg_iters_per_newton": pcg / max(newton, 1),
-        "phase_ms_per_frame": {k: sum(s[k] for s in stats) / args.steps for k in
-                               ("ms_collision", "ms_assembly", "ms_pcg", "ms_linesearch", "ms_total")},
-        "max_constraints": max(s["max_constraints"] for s in stats),
+                   "l2": "inputs larger than L2 (system ~0.5 GB/PCG iteration)"},
+        "pcg_iters_per_s_in_pcg": pcg / (d["ms_pcg"] / 1000.0) if d["ms_pcg"] > 0 else None,
+        "newton_iters": newton, "pcg_iters": pcg, "pcg_iters_per_newton": ppn,
+        "ms_per_newton": ms_newton,
+        "phase_ms_per_newton": {k: d[k] / max(newton, 1) for k in
+                                ("ms_collision", "ms_assembly", "ms_pcg", "ms_linesearch")},
+        "frames_completed_in_timed_region": len(new_frames),
+        "frames_hit_newton_cap": run.unconverged,
+        "seconds_per_frame": (float(np.mean([f[0] for f in new_frames])) / 1000.0) if new_frames else None,
+        "seconds_per_frame_projection": (ms_newton * npf_ref / 1000.0) if npf_ref else None,
+        "newton_per_frame_ref": npf_ref,
+        "max_constraints": tot1["max_constraints"],
         "roofline": {"kernel": "k_spmv (BSR3 SpMV in PCG)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src, "mean_launch_us": spmv_us, "launches": d_n,
-                     "alg_bytes_per_launch": d_alg / max(d_n, 1), "full_bsr_bytes_per_launch": d_mov / max(d_n, 1),
-                     "full_bsr_gbs": moved_gbs},
+                     "alg_bytes_per_launch": d_alg / max(d_n, 1), "kernel_min_bytes_per_launch": d_mov / max(d_n, 1),
+                     "kernel_min_gbs": moved_gbs},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

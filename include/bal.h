@@ -111,6 +111,19 @@ bal_status bal_set_stream(bal_ctx* ctx, void* cuda_stream);
 bal_status bal_step(bal_ctx* ctx, const double* x_t, const double* v_t, double* x_next,
                     double* v_next, bal_step_stats* stats);
 
+/* bal_step in slices (same computation, same results): bal_frame_begin does the step setup
+ * (predictor y, constraint set at x_t, sigma^0; Alg. 1 lines before the loop, Q7);
+ * bal_frame_iterate runs up to max_iters further inexact-Newton iterations of Alg. 1 (one l =
+ * assembly + warm start + PCG + CCD line search + AL updates, Q6) and sets *converged = 1 once
+ * the P:261 test passed; bal_frame_finish writes x_{t+1}, v_{t+1} (device [3N]; either may be
+ * NULL) and the stats.  bal_step == begin + iterate(max_newton) + finish.  Errors as bal_step;
+ * BAL_E_INVALID_ARG when no frame is in progress.  x_t, v_t are read only during begin. */
+bal_status bal_frame_begin(bal_ctx* ctx, const double* x_t, const double* v_t);
+bal_status bal_frame_iterate(bal_ctx* ctx, int32_t max_iters, int32_t* converged);
+bal_status bal_frame_finish(bal_ctx* ctx, double* x_next, double* v_next, bal_step_stats* stats);
+/* Stats of the frame in progress so far (counts and per-phase ms accumulated since begin). */
+bal_status bal_frame_peek(const bal_ctx* ctx, bal_step_stats* stats);
+
 /* End-to-end variant of bal_step: x_t, v_t, x_next, v_next are HOST arrays [3N]; the
  * host<->device copies are part of the call (used for the e2e measurement). */
 bal_status bal_step_host(bal_ctx* ctx, const double* x_t, const double* v_t, double* x_next,

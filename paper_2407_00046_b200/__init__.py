@@ -132,6 +132,38 @@ def bal_step(ctx, x_t, v_t, x_next, v_next=None):
     return {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
 
 
+def bal_frame_begin(ctx, x_t, v_t):
+    """Start a time step (setup of Alg. 1) on device tensors; advance it with bal_frame_iterate."""
+    _check(ctx, _lib.lib.bal_frame_begin(ctx.handle, _dptr(x_t), _dptr(v_t)))
+
+
+def bal_frame_iterate(ctx, max_iters):
+    """Run up to max_iters inexact-Newton iterations of the frame in progress; True once converged."""
+    done = C.c_int32(0)
+    _check(ctx, _lib.lib.bal_frame_iterate(ctx.handle, int(max_iters), C.byref(done)))
+    return bool(done.value)
+
+
+def bal_frame_finish(ctx, x_next=None, v_next=None, allow_unconverged=False):
+    """Write x_{t+1}, v_{t+1} of the frame in progress; returns the stats dict.  Raises BalError on
+    BAL_E_NOT_CONVERGED unless allow_unconverged (x_next is the last accepted iterate either way)."""
+    s = bal_step_stats()
+    st = _lib.lib.bal_frame_finish(ctx.handle, _dptr(x_next), _dptr(v_next), C.byref(s))
+    out = {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
+    out["converged"] = st == 0
+    if st == -4 and allow_unconverged:
+        return out
+    _check(ctx, st)
+    return out
+
+
+def bal_frame_stats(ctx):
+    """Stats of the frame in progress so far (same fields as bal_step's), without finishing it."""
+    s = bal_step_stats()
+    _check(ctx, _lib.lib.bal_frame_peek(ctx.handle, C.byref(s)))
+    return {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
+
+
 def bal_step_host(ctx, x_t, v_t):
     """End-to-end step on host numpy arrays (copies inside the call)."""
     x_t = np.ascontiguousarray(x_t, np.float64).ravel()

@@ -93,6 +93,10 @@ _sig = {
     "bal_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_step_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p,
                                 C.POINTER(bal_step_stats)]),
+    "bal_frame_begin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "bal_frame_iterate": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]),
+    "bal_frame_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_step_stats)]),
+    "bal_frame_peek": (C.c_int, [C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(bal_contact_state), C.POINTER(bal_system_view)]),
     "bal_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bal_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_pcg_opts),

@@ -55,6 +55,8 @@ struct ContactWork {
   DevBuf<unsigned char> tmp;
   DevBuf<int> row_ptr, col;
   DevBuf<double> val;
+  DevBuf<int> split, tpos, mflag;  // symmetric-SpMV mirror index (kernels.h Bsr)
+  bool sym = false;
   int nslots = 0;
   int nrows = 0;  // non-empty contact rows (= contact diagonal slots)
 };

@@ -18,11 +18,19 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.row_ptr = lb_row_ptr.ptr;
     b.col = lb_col.ptr;
     b.val = lb_val.ptr;
+    if (lb_sym) {
+      b.split = lb_split.ptr;
+      b.tpos = lb_tpos.ptr;
+    }
   } else {
     b.nnzb = sp.nnzb;
     b.row_ptr = sp.row_ptr;
     b.col = sp.col;
     b.val = sval.ptr;
+    if (sp_sym) {
+      b.split = sp_split.ptr;
+      b.tpos = sp_tpos.ptr;
+    }
   }
   return b;
 }
@@ -34,6 +42,10 @@ bal::Bsr bal_ctx::contact_bsr() const {
   b.row_ptr = cw.row_ptr.ptr;
   b.col = cw.col.ptr;
   b.val = cw.val.ptr;
+  if (cw.sym) {
+    b.split = cw.split.ptr;
+    b.tpos = cw.tpos.ptr;
+  }
   return b;
 }
 
@@ -298,6 +310,11 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->sp.diag_pos = c->sp_diag_pos.ptr;
   c->sp.slot_ptr = c->sp_slot_ptr.ptr;
   c->sp.slot_code = c->sp_slot_code.ptr;
+  c->sp_split.reserve(N);
+  c->sp_tpos.reserve(nnzb);
+  c->mflag.reserve(1);
+  c->sp_sym = spmv_symmetric_enabled() &&
+              build_mirror(st, N, nnzb, c->sp.row_ptr, c->sp.col, c->sp_split.ptr, c->sp_tpos.ptr, c->mflag.ptr);
   c->sval.reserve(9 * (size_t)nnzb);
   c->stage_e.reserve(90 * (size_t)std::max(T, 1));
   c->grad_e.reserve(12 * (size_t)std::max(T, 1));
@@ -496,6 +513,12 @@ bal_status bal_load_bsr(bal_ctx* c, const bal_bsr_host* b) {
     c->lb_val.upload(b->val, 9 * (size_t)b->nnzb, st);
     c->lb_nnzb = b->nnzb;
     c->loaded_bsr = true;
+    c->lb_split.reserve(c->N);
+    c->lb_tpos.reserve(std::max(b->nnzb, 1));
+    c->mflag.reserve(1);
+    c->lb_sym = spmv_symmetric_enabled() && b->nnzb > 0 &&
+                build_mirror(st, c->N, b->nnzb, c->lb_row_ptr.ptr, c->lb_col.ptr, c->lb_split.ptr, c->lb_tpos.ptr,
+                             c->mflag.ptr);
     // diagonal inverse from the loaded blocks (host: test path only)
     std::vector<double> dinv(6 * (size_t)c->N, 0.0);
     for (int i = 0; i < c->N; ++i) {

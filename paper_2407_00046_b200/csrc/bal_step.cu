@@ -27,6 +27,14 @@ struct StepWork {
   DevBuf<double> evals, esc;  // per-item energies, energy scalars
   DevBuf<int> sel, selcnt;
   DevBuf<unsigned char> tmp;
+  // state of the frame in progress (Alg. 1 loop variables), so the loop can be advanced in slices
+  struct Frame {
+    bool active = false, converged = false;
+    int l = 0;
+    double sigma = 0, sig0 = 0, dmin = 0, dmin_prev = 0, e0 = -1;
+    bal_step_stats S{};
+    std::chrono::steady_clock::time_point t_start;
+  } fr;
 };
 
 void destroy_step_work(bal_ctx* c) {
@@ -385,28 +393,34 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
-bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_next, double* v_next,
-                   bal_step_stats* stats) {
+// ---- Alg. 1 split into frame setup / Newton iterations / finish so callers (bench)
+// can advance a frame in slices of Newton iterations; bal_step = begin + iterate(max_newton) + finish.
+static bool verbose_on() {
+  static const bool v = getenv("BAL_VERBOSE") != nullptr;
+  return v;
+}
+static void vmark(bal_ctx* c, std::chrono::steady_clock::time_point& t_mark, const char* what, long long a = -1,
+                  long long b = -1) {
+  if (!verbose_on()) return;
+  CK(cudaStreamSynchronize(c->st));
+  fprintf(stderr, "[bal]   %-12s %9.2f ms  %lld %lld\n", what, ms_since(t_mark), a, b);
+  t_mark = std::chrono::steady_clock::now();
+}
+
+void frame_begin(bal_ctx* c, const double* x_t, const double* v_t) {
   using clk = std::chrono::steady_clock;
-  const auto t_start = clk::now();
   if (!c->sw) c->sw = new StepWork();
   StepWork& w = *c->sw;
+  StepWork::Frame& F = w.fr;
+  F = StepWork::Frame();
+  F.t_start = clk::now();
   cudaStream_t st = c->st;
   const int N = c->N;
   const size_t n3 = 3 * (size_t)N;
   const bal_params& P = c->prm;
-  const double h = P.h, dhat = P.dhat;
-  bal_step_stats S;
-  std::memset(&S, 0, sizeof(S));
+  const double h = P.h;
   c->trace.clear();
-  static const bool verbose = getenv("BAL_VERBOSE") != nullptr;
   auto t_mark = clk::now();
-  auto mark = [&](const char* what, long long a = -1, long long b = -1) {
-    if (!verbose) return;
-    CK(cudaStreamSynchronize(st));
-    fprintf(stderr, "[bal]   %-12s %9.2f ms  %lld %lld\n", what, ms_since(t_mark), a, b);
-    t_mark = clk::now();
-  };
   for (auto* b : {&w.x, &w.xn, &w.dir, &w.rhs, &w.trial, &w.v}) b->reserve(n3);
   CK(cudaMemcpyAsync(c->xt.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   k_predictor<<<ceil_div(N, 256), 256, 0, st>>>(N, x_t, v_t, h, P.gravity[0], P.gravity[1], P.gravity[2],
@@ -414,23 +428,52 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
   CK(cudaMemcpyAsync(w.x.ptr, x_t, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   w.n_ap = 0;
   c->n_fric = 0;
-  mark("setup");
+  vmark(c, t_mark, "setup");
   auto t0 = clk::now();
   proximity(c, w, w.x.ptr);
-  mark("proximity", w.cand_prox.npt + w.cand_prox.nee, w.cs_A.n);
-  double dmin = min_d(c, w, w.cs_A);
-  S.ms_collision += ms_since(t0);
-  if (!(dmin > 0.0)) throw StepFail(BAL_E_INFEASIBLE, "bal_step: input has a surface distance <= 0");
+  vmark(c, t_mark, "proximity", w.cand_prox.npt + w.cand_prox.nee, w.cs_A.n);
+  F.dmin = min_d(c, w, w.cs_A);
+  F.S.ms_collision += ms_since(t0);
+  if (!(F.dmin > 0.0)) throw StepFail(BAL_E_INFEASIBLE, "bal_step: input has a surface distance <= 0");
   t0 = clk::now();
-  const double sig0 = sigma0(c, w, w.x.ptr);
-  mark("sigma0");
-  S.ms_assembly += ms_since(t0);
-  double sigma = sig0;
-  double dmin_prev = INFINITY;
-  double e0 = -1.0;
-  bool converged = false;
+  F.sig0 = sigma0(c, w, w.x.ptr);
+  vmark(c, t_mark, "sigma0");
+  F.S.ms_assembly += ms_since(t0);
+  F.sigma = F.sig0;
+  F.dmin_prev = INFINITY;
+  F.e0 = -1.0;
+  F.converged = false;
+  F.l = 0;
+  F.active = true;
+}
+
+// Runs up to max_iters Newton iterations of the frame in progress; returns true once converged.
+bool frame_iterate(bal_ctx* c, int max_iters) {
+  using clk = std::chrono::steady_clock;
+  if (!c->sw || !c->sw->fr.active) throw StepFail(BAL_E_INVALID_ARG, "bal_frame_iterate: no frame in progress");
+  StepWork& w = *c->sw;
+  StepWork::Frame& F = w.fr;
+  if (F.converged) return true;
+  if (F.l >= c->prm.max_newton) throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: Newton iteration cap reached");
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  const bal_params& P = c->prm;
+  const double dhat = P.dhat;
+  const bool verbose = verbose_on();
+  auto t_mark = clk::now();
+  auto mark = [&](const char* what, long long a = -1, long long b = -1) { vmark(c, t_mark, what, a, b); };
+  bal_step_stats& S = F.S;
+  double& sigma = F.sigma;
+  double& dmin = F.dmin;
+  double& dmin_prev = F.dmin_prev;
+  double& e0 = F.e0;
+  const double sig0 = F.sig0;
+  const auto t_start = F.t_start;
   const bool no_al = (P.flags & BAL_NO_AUGLAG) != 0;
-  for (int l = 0; l < P.max_newton; ++l) {
+  auto t0 = clk::now();
+  const int l_end = std::min(P.max_newton, F.l + std::max(max_iters, 0));
+  for (; F.l < l_end; ++F.l) {
+    const int l = F.l;
     if (l > 0) {
       t0 = clk::now();
       proximity(c, w, w.x.ptr);
@@ -474,8 +517,9 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
     S.ms_assembly += ms_since(t0);
     if (e0 < 0) e0 = en;
     if (e0 == 0.0) {
-      converged = true;
-      break;
+      F.converged = true;
+      ++F.l;
+      return true;
     }
     // Newton direction: A p = -e with warm start + PCG (App. B)
     launch_axpy(st, 3 * N, -2.0, c->grad.ptr, c->grad.ptr, w.rhs.ptr);  // rhs = e - 2e = -e
@@ -551,8 +595,9 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
     // x^{l+1} is in w.trial; its constraint set is w.cs_trial
     if (en <= P.newton_rel_tol * e0) {
       std::swap(w.x.ptr, w.trial.ptr);
-      converged = true;
-      break;
+      F.converged = true;
+      ++F.l;
+      return true;
     }
     if (w.n_ap > 0) {  // Alg. 1 lines 12-14
       w.ap_d.reserve(w.n_ap);
@@ -566,16 +611,44 @@ bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_n
     }
     std::swap(w.x.ptr, w.trial.ptr);
   }
+  return F.converged;
+}
+
+void frame_finish(bal_ctx* c, double* x_next, double* v_next, bal_step_stats* stats) {
+  if (!c->sw || !c->sw->fr.active) throw StepFail(BAL_E_INVALID_ARG, "bal_frame_finish: no frame in progress");
+  StepWork& w = *c->sw;
+  StepWork::Frame& F = w.fr;
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  const size_t n3 = 3 * (size_t)N;
   k_restore_fixed<<<ceil_div(N, 256), 256, 0, st>>>(N, c->xt.ptr, c->fixed.ptr, w.x.ptr);
-  CK(cudaMemcpyAsync(x_next, w.x.ptr, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  if (v_next) k_velocity<<<ceil_div((int)n3, 256), 256, 0, st>>>((int)n3, w.x.ptr, c->xt.ptr, 1.0 / h, v_next);
+  if (x_next) CK(cudaMemcpyAsync(x_next, w.x.ptr, n3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (v_next) k_velocity<<<ceil_div((int)n3, 256), 256, 0, st>>>((int)n3, w.x.ptr, c->xt.ptr, 1.0 / c->prm.h, v_next);
   CK(cudaStreamSynchronize(st));
-  S.sigma0 = sig0;
-  S.sigma_final = sigma;
-  S.min_distance = dmin;
-  S.ms_total = ms_since(t_start);
-  if (stats) *stats = S;
-  if (!converged) throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: Newton iteration cap reached");
+  F.S.sigma0 = F.sig0;
+  F.S.sigma_final = F.sigma;
+  F.S.min_distance = F.dmin;
+  F.S.ms_total = ms_since(F.t_start);
+  if (stats) *stats = F.S;
+  F.active = false;
+  if (!F.converged) throw StepFail(BAL_E_NOT_CONVERGED, "bal_step: Newton iteration cap reached");
+}
+
+bal_status do_step(bal_ctx* c, const double* x_t, const double* v_t, double* x_next, double* v_next,
+                   bal_step_stats* stats) {
+  frame_begin(c, x_t, v_t);
+  try {
+    frame_iterate(c, c->prm.max_newton);
+  } catch (const StepFail&) {
+    // line-search failure: x_next = last accepted iterate (still intersection-free), then report it
+    c->sw->fr.converged = false;
+    try {
+      frame_finish(c, x_next, v_next, stats);
+    } catch (const StepFail&) {
+    }
+    throw;
+  }
+  frame_finish(c, x_next, v_next, stats);
   return BAL_OK;
 }
 
@@ -622,6 +695,41 @@ bal_status bal_step_host(bal_ctx* c, const double* x_t, const double* v_t, doubl
     CK(cudaStreamSynchronize(c->st));
     return s;
   });
+}
+
+bal_status bal_frame_begin(bal_ctx* c, const double* x_t, const double* v_t) {
+  if (!c || !x_t || !v_t) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() {
+    frame_begin(c, x_t, v_t);
+    return BAL_OK;
+  });
+}
+
+bal_status bal_frame_iterate(bal_ctx* c, int32_t max_iters, int32_t* converged) {
+  if (!c || max_iters < 0) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() {
+    const bool done = frame_iterate(c, max_iters);
+    if (converged) *converged = done ? 1 : 0;
+    return BAL_OK;
+  });
+}
+
+bal_status bal_frame_finish(bal_ctx* c, double* x_next, double* v_next, bal_step_stats* stats) {
+  if (!c) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() {
+    frame_finish(c, x_next, v_next, stats);
+    return BAL_OK;
+  });
+}
+
+bal_status bal_frame_peek(const bal_ctx* c, bal_step_stats* stats) {
+  if (!c || !stats || !c->sw || !c->sw->fr.active) return BAL_E_INVALID_ARG;
+  *stats = c->sw->fr.S;
+  stats->sigma0 = c->sw->fr.sig0;
+  stats->sigma_final = c->sw->fr.sigma;
+  stats->min_distance = c->sw->fr.dmin;
+  stats->ms_total = ms_since(c->sw->fr.t_start);
+  return BAL_OK;
 }
 
 int32_t bal_get_trace(const bal_ctx* c, double* out, int32_t max_records) {

@@ -11,6 +11,7 @@
 
 #include "assemble.h"
 #include "common.cuh"
+#include "kernels.h"
 
 namespace bal {
 
@@ -283,6 +284,13 @@ int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* no
   k_count_rows<<<ceil_div(n, 256), 256, 0, st>>>(n, w.row_ptr.ptr, w.nvalid.ptr);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&w.nrows, w.nvalid.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  w.sym = false;
+  if (nslots > 0 && spmv_symmetric_enabled()) {
+    w.split.reserve(n);
+    w.tpos.reserve(nslots);
+    w.mflag.reserve(1);
+    w.sym = build_mirror(st, n, nslots, w.row_ptr.ptr, w.col.ptr, w.split.ptr, w.tpos.ptr, w.mflag.ptr);
+  }
   return nslots;
 }
 

@@ -23,47 +23,45 @@ constexpr int kSL = 16;        // lanes per block row
 constexpr int kSpmvThreads = 256;
 constexpr int kSpmvBlocks = 16 * kSMs;
 
+// Lane mapping: a 16-lane half-warp owns one block row; its lanes 0..11 form 4 block slots x 3
+// component rows (q = lane/3, r = lane%3), lanes 12..15 idle.  Per pass the half-warp consumes 4
+// blocks of the row: lane (q, r) multiplies row r of block q (or column r when the block is the
+// mirror A_ji of an upper slot, i.e. (A_ji)^T) with the 3 components of v at the block's column
+// and accumulates one scalar y_r.  A row's result is two shuffles away (strides 6 and 3).  Each
+// lane's three value loads read 24 contiguous bytes; the 12 lanes read a block's 72 bytes whole.
+constexpr int kLanesPerRow = 12;
+constexpr int kBlocksPerPass = kLanesPerRow / 3;
+
 template <bool MASK>
-BAL_D void row_accum(const Bsr& A, int row, int lane, const double* __restrict__ v, const int* __restrict__ grp,
-                     int gr, double& a0, double& a1, double& a2) {
+BAL_D double row_accum(const Bsr& A, int row, int q, int r, const double* __restrict__ v, const int* __restrict__ grp,
+                       int gr) {
   const int beg = __ldg(A.row_ptr + row), end = __ldg(A.row_ptr + row + 1);
-  const double* __restrict__ vals = A.val + 9 * (size_t)beg;
-  const int* __restrict__ cols = A.col + beg;
-  const unsigned nf = 9u * (unsigned)(end - beg);
-  // kU independent element loads in flight per lane (memory-level parallelism): the row's values
-  // are contiguous, so each unrolled load is a fully coalesced 128 B access of the sub-warp
-  constexpr int kU = 4;
-  for (unsigned f0 = lane; f0 < nf; f0 += kU * kSL) {
-    double a[kU], xv[kU];
-    unsigned rr[kU];
-#pragma unroll
-    for (int j = 0; j < kU; ++j) {
-      const unsigned f = f0 + j * kSL;
-      a[j] = 0.0;
-      rr[j] = 0;
-      if (f < nf) a[j] = __ldcs(vals + f);  // streamed once per SpMV: evict-first
+  const int split = A.tpos ? __ldg(A.split + row) : end;
+  double acc = 0.0;
+#pragma unroll 2
+  for (int s = beg + q; s < end; s += kBlocksPerPass) {
+    const bool up = s >= split;
+    const int blk = up ? __ldg(A.tpos + s) : s;
+    const int col = __ldg(A.col + s);
+    double x0 = __ldg(v + 3 * (size_t)col), x1 = __ldg(v + 3 * (size_t)col + 1),
+           x2 = __ldg(v + 3 * (size_t)col + 2);
+    if (MASK && __ldg(grp + col) != gr) x0 = x1 = x2 = 0.0;
+    const double* __restrict__ a = A.val + 9 * (size_t)blk;
+    double a0, a1, a2;
+    if (up) {  // column r of the mirror block A_ji (read through L2; an earlier row streamed it)
+      a0 = __ldg(a + r);
+      a1 = __ldg(a + 3 + r);
+      a2 = __ldg(a + 6 + r);
+    } else {  // row r of this row's own block, streamed once: evict-first
+      a0 = __ldcs(a + 3 * r);
+      a1 = __ldcs(a + 3 * r + 1);
+      a2 = __ldcs(a + 3 * r + 2);
     }
-#pragma unroll
-    for (int j = 0; j < kU; ++j) {
-      const unsigned f = f0 + j * kSL;
-      xv[j] = 0.0;
-      if (f < nf) {
-        const unsigned blk = f / 9u, rem = f - 9u * blk;
-        const unsigned r = rem / 3u, c = rem - 3u * r;
-        const int col = __ldg(cols + blk);
-        xv[j] = __ldg(v + 3 * (size_t)col + c);
-        if (MASK && __ldg(grp + col) != gr) xv[j] = 0.0;
-        rr[j] = r;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kU; ++j) {
-      const double pr = a[j] * xv[j];
-      if (rr[j] == 0) a0 += pr;
-      else if (rr[j] == 1) a1 += pr;
-      else a2 += pr;
-    }
+    acc = fma(a0, x0, acc);
+    acc = fma(a1, x1, acc);
+    acc = fma(a2, x2, acc);
   }
+  return acc;
 }
 
 template <bool DOT, bool MASK>
@@ -73,6 +71,8 @@ k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, 
   if (DOT && sc->done) return;
   const int n = S.n;
   const int lane = threadIdx.x & (kSL - 1);
+  const int q = lane / 3, r = lane - 3 * (lane / 3);
+  const bool active_lane = lane < kLanesPerRow;
   const int sub_in_warp = (threadIdx.x & 31) / kSL;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -80,28 +80,23 @@ k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, 
   double dacc = 0.0;
   for (int base = gwarp * kRowsPerWarp; base < n; base += nwarps * kRowsPerWarp) {
     const int row = base + sub_in_warp;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    double acc = 0.0;
     bool valid = row < n;
     int gr = 0;
     if (MASK && valid) {
       gr = grp[row];
       valid = gr >= 0 && gs->active[gr];
     }
-    if (valid) {
-      row_accum<MASK>(S, row, lane, v, grp, gr, a0, a1, a2);
-      if (C.nnzb > 0) row_accum<MASK>(C, row, lane, v, grp, gr, a0, a1, a2);
+    if (valid && active_lane) {
+      acc = row_accum<MASK>(S, row, q, r, v, grp, gr);
+      if (C.nnzb > 0) acc += row_accum<MASK>(C, row, q, r, v, grp, gr);
     }
-#pragma unroll
-    for (int o = kSL / 2; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-    }
-    if (valid && lane == 0) {
-      y[3 * (size_t)row] = a0;
-      y[3 * (size_t)row + 1] = a1;
-      y[3 * (size_t)row + 2] = a2;
-      if (DOT) dacc += v[3 * (size_t)row] * a0 + v[3 * (size_t)row + 1] * a1 + v[3 * (size_t)row + 2] * a2;
+    // lanes r, r+3, r+6, r+9 of the half-warp hold the partial sums of component r
+    acc += __shfl_down_sync(0xffffffffu, acc, 6, kSL);
+    acc += __shfl_down_sync(0xffffffffu, acc, 3, kSL);
+    if (valid && lane < 3) {
+      y[3 * (size_t)row + lane] = acc;
+      if (DOT) dacc += v[3 * (size_t)row + lane] * acc;
     }
   }
   if (DOT) {
@@ -147,6 +142,42 @@ void launch_spmv_masked(cudaStream_t st, const Bsr& S, const Bsr& C, const int* 
   const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
   k_spmv<false, true><<<blocks, kSpmvThreads, 0, st>>>(S, C, grp, v, y, nullptr, nullptr, nullptr, gs);
   CK(cudaGetLastError());
+}
+
+// mirror index: split[i] = first slot of row i with col > i; tpos[s] = slot of (col[s], i)
+__global__ void k_bsr_mirror(int n, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                             int* __restrict__ split, int* __restrict__ tpos, int* bad) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int beg = row_ptr[i], end = row_ptr[i + 1];
+  int sp = end;
+  for (int s = beg; s < end; ++s) {
+    const int j = col[s];
+    if (s > beg && col[s - 1] >= j) atomicExch(bad, 1);  // rows must be strictly column-sorted
+    if (j > i && sp == end) sp = s;
+    int lo = row_ptr[j], hi = row_ptr[j + 1];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (col[mid] < i) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < row_ptr[j + 1] && col[lo] == i) tpos[s] = lo;
+    else atomicExch(bad, 1);
+  }
+  split[i] = sp;
+}
+
+bool build_mirror(cudaStream_t st, int n, int nnzb, const int* row_ptr, const int* col, int* split, int* tpos,
+                  int* flag_dev) {
+  if (n <= 0) return false;
+  CK(cudaMemsetAsync(flag_dev, 0, sizeof(int), st));
+  k_bsr_mirror<<<ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, col, split, tpos, flag_dev);
+  CK(cudaGetLastError());
+  int bad = 1;
+  CK(cudaMemcpyAsync(&bad, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  (void)nnzb;
+  return bad == 0;
 }
 
 // ---------------------------------------------------------------------------------- vectors

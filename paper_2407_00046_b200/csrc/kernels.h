@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace bal {
 
@@ -31,7 +32,21 @@ struct Bsr {
   const int* row_ptr = nullptr;
   const int* col = nullptr;
   const double* val = nullptr;
+  // symmetric mode (both set): row i streams only its slots [row_ptr[i], split[i]) (lower blocks +
+  // diagonal) and applies each upper slot s in [split[i], row_ptr[i+1]) as the transpose of its
+  // mirror block val[tpos[s]] = A_ji -- every off-diagonal block leaves HBM once (the
+  // paper's D + L + L^T storage) and the mirror read hits L2.  Null = stream every stored block.
+  const int* split = nullptr;  // [n]
+  const int* tpos = nullptr;   // [nnzb]
 };
+// mirror index of a pattern-symmetric BSR with column-sorted rows: split[i], tpos[s]; returns
+// false (no symmetric mode) when a slot has no mirror
+inline bool spmv_symmetric_enabled() {
+  static const bool full = getenv("BAL_SPMV_FULL") != nullptr;  // A/B switch: stream both triangles
+  return !full;
+}
+bool build_mirror(cudaStream_t st, int n, int nnzb, const int* row_ptr, const int* col, int* split, int* tpos,
+                  int* flag_dev);
 
 // PCG scalars living in device memory (single group)
 struct PcgScal {

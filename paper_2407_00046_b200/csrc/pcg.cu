@@ -70,15 +70,15 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
   for (int it = 0; it < kBatch; ++it) {
     // CUDA events bracket every SpMV launch: the bench reports the SpMV kernel's average duration
     // inside the timed region from these (roofline achieved GB/s)
-    CK(cudaEventRecord(ev[2 * it], st));
+    CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
     launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
-    CK(cudaEventRecord(ev[2 * it + 1], st));
+    CK(cudaEventRecordWithFlags(ev[2 * it + 1], st, cudaEventRecordExternal));
     launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
                       c->counter.ptr, c->scal.ptr, c->hist.ptr);
     launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
   }
   CK(cudaMemcpyAsync(c->h_scal + 1 + set, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
-  CK(cudaEventRecord(ev[2 * kBatch], st));
+  CK(cudaEventRecordWithFlags(ev[2 * kBatch], st, cudaEventRecordExternal));
   CK(cudaStreamEndCapture(st, &g));
   CK(cudaGraphInstantiate(out, g, 0));
   CK(cudaGraphDestroy(g));

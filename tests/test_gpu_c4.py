@@ -1,0 +1,123 @@
+"""GPU parity at BASELINE.json's full size (configs[3], the C4 puffer-net scene, ~1.75M tets) in the
+launch configuration bench.py times: sampled outputs the oracle computes one by one (elastic
+stencils of sampled tets, assembled rows of sampled nodes), the SpMV against the CSR product of the
+assembled blocks over every row, and fixed-iteration PCG against the oracle's textbook PCG on the
+same (GPU-assembled) system.  SURVEY §8(c) c.4; tolerances as north_star states."""
+import numpy as np
+import pytest
+
+import scenes
+from tests.gpu_helpers import bsr_to_csr, dinv_full, lower_blocks_to_full
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2407_00046_b200 as bal  # noqa: E402
+from oracle import linalg as la  # noqa: E402
+from oracle.energy import nh_stencils  # noqa: E402
+from oracle.mesh import precompute  # noqa: E402
+from oracle.projection import lambda_bar, project_eigh  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a, np.float64).ravel(), device=DEV)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def c4():
+    sc = scenes.make_puffer_net(seed=4)
+    m = precompute(sc)
+    rng = np.random.default_rng(44)
+    # a deformed, generic configuration: small random displacement of every free node
+    x = sc["x0"] + 2e-4 * rng.normal(size=sc["x0"].shape) * (1 - sc["node_fixed"][:, None])
+    p = sc["params"]
+    y = x + p["h"] * sc["v0"] + p["h"] ** 2 * np.array(p["gravity"])[None]
+    ctx = bal.bal_init(sc)
+    out = bal.bal_assemble(ctx, _t(x), y=y)
+    A = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), len(x))
+    return sc, m, x, y, ctx, out, A
+
+
+def _sub_mesh(m, sel):
+    return type(m)(**{**m.__dict__, "tets": m.tets[sel], "Dm_inv": m.Dm_inv[sel], "vol": m.vol[sel],
+                      "mu": m.mu[sel], "lam": m.lam[sel]})
+
+
+def test_c4_sampled_elastic_stencils(c4):
+    sc, m, x, y, ctx, out, A = c4
+    rng = np.random.default_rng(1)
+    sel = np.sort(rng.choice(len(m.tets), size=3000, replace=False))
+    _v, _g, H = nh_stencils(x, _sub_mesh(m, sel))
+    P, _ = project_eigh(H)
+    lb = lambda_bar(P)
+    Pg = _np(out["elastic_blocks"]).reshape(-1, 90)[sel]
+    err = max(np.linalg.norm(lower_blocks_to_full(Pg[i], 4) - P[i]) / max(np.linalg.norm(P[i]), 1e-300)
+              for i in range(len(sel)))
+    assert err <= 1e-12, err
+    np.testing.assert_allclose(_np(out["elastic_lbar"])[sel], lb, rtol=1e-12, atol=0)
+
+
+def test_c4_sampled_assembled_rows(c4):
+    """Rows of sampled free nodes: M/h^2 + sum over incident tets of S^T P(H) S, summed densely."""
+    sc, m, x, y, ctx, out, A = c4
+    rng = np.random.default_rng(2)
+    N = len(x)
+    free = np.flatnonzero(sc["node_fixed"] == 0)
+    nodes = rng.choice(free, size=150, replace=False)
+    p = sc["params"]
+    flat = m.tets.ravel()
+    order = np.argsort(flat, kind="stable")
+    starts = np.searchsorted(flat[order], np.arange(N + 1))
+    for i in nodes:
+        tsel = np.unique(order[starts[i]:starts[i + 1]] // 4)
+        _v, _g, H = nh_stencils(x, _sub_mesh(m, tsel))
+        P, _ = project_eigh(H)
+        row = np.zeros((3, 3 * N))
+        row[:, 3 * i:3 * i + 3] += np.eye(3) * m.mass[i] / p["h"] ** 2
+        for t, e in enumerate(tsel):
+            a = int(np.flatnonzero(m.tets[e] == i)[0])
+            for b in range(4):
+                j = m.tets[e, b]
+                if sc["node_fixed"][j]:
+                    continue  # fixed DOFs: identity rows/columns (App. C, Q23)
+                row[:, 3 * j:3 * j + 3] += P[t][3 * a:3 * a + 3, 3 * b:3 * b + 3]
+        g = A[3 * i:3 * i + 3].toarray()
+        scale = np.abs(row).sum()
+        assert np.abs(g - row).sum() <= 1e-12 * scale, i
+
+
+def test_c4_spmv_every_row(c4):
+    sc, m, x, y, ctx, out, A = c4
+    rng = np.random.default_rng(3)
+    v = rng.normal(size=A.shape[0])
+    yg = torch.empty(A.shape[0], dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    yo = A @ v
+    bound = abs(A) @ np.abs(v)
+    assert np.all(np.abs(_np(yg) - yo) <= 1e-12 * bound + 1e-300)
+    # bitwise deterministic run to run
+    y2 = torch.empty_like(yg)
+    bal.bal_spmv(ctx, _t(v), y2)
+    assert torch.equal(yg, y2)
+
+
+def test_c4_pcg_fixed_iterations(c4):
+    """k textbook block-Jacobi PCG iterations (no stopping) from x0 = 0 on the assembled C4 system."""
+    sc, m, x, y, ctx, out, A = c4
+    b = -_np(out["grad"])
+    Dinv = dinv_full(_np(out["diag_inv"]))
+    xg = torch.empty(A.shape[0], dtype=torch.float64, device=DEV)
+    k = 12
+    s = bal.bal_pcg(ctx, _t(b), _t(np.zeros_like(b)), xg, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=k)
+    st = la.pcg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+    assert s["iters"] == k == st.k
+    assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)

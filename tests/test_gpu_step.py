@@ -116,3 +116,26 @@ def test_sliding_tet_with_friction_parity():
     xo, to = oracle_steps(sc, 4)
     for k in range(4):
         assert _rel(xg[k], xo[k], xo[k] - sc["x0"]) <= 1e-6, k
+
+
+def test_frame_slices_equal_bal_step():
+    """bal_frame_begin + bal_frame_iterate(1) x n + bal_frame_finish == bal_step, bitwise (the bench
+    advances frames one Newton iteration per step)."""
+    sc = scenes.make_cubes(1)
+    xg, tg, sg = gpu_steps(sc, 2)
+    ctx = bal.bal_init(sc)
+    x = torch.as_tensor(sc["x0"].ravel(), device=DEV)
+    v = torch.as_tensor(sc["v0"].ravel(), device=DEV)
+    for k in range(2):
+        xn, vn = torch.empty_like(x), torch.empty_like(v)
+        bal.bal_frame_begin(ctx, x, v)
+        n = 0
+        while not bal.bal_frame_iterate(ctx, 1):
+            n += 1
+            assert bal.bal_frame_stats(ctx)["newton_iters"] == n
+        st = bal.bal_frame_finish(ctx, xn, vn)
+        assert st["newton_iters"] == sg[k]["newton_iters"] and st["pcg_iters"] == sg[k]["pcg_iters"]
+        assert np.array_equal(xn.cpu().numpy().reshape(-1, 3), xg[k])
+        x, v = xn, vn
+    with pytest.raises(bal.BalError):
+        bal.bal_frame_iterate(ctx, 1)  # no frame in progress
