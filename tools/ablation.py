@@ -1,0 +1,60 @@
+"""NEXT-1 ablations on the same kernels: warm start on/off (Fig. warm
+start), BAL vs plain inexact-Newton IPC (A' = empty, sigma = sigma^0).  Runs whole frames of
+a scene through bal_frame_* with each flag set and prints per-variant totals as JSON lines.
+
+    python tools/ablation.py c1 [frames]            # C1 cubes, all frames
+    python tools/ablation.py c4 [newton_iters]      # C4: the first K Newton iterations of frame 0
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2407_00046_b200 as bal  # noqa: E402
+import scenes  # noqa: E402
+
+VARIANTS = {"bal+warmstart": 0, "bal, no warm start": bal.BAL_NO_WARMSTART,
+            "inexact Newton (no AL)": bal.BAL_NO_AUGLAG}
+
+
+def run(sc, flags, frames=None, newton=None):
+    dev = torch.device("cuda:0")
+    ctx = bal.bal_init(sc, flags=flags)
+    st = torch.cuda.current_stream(dev)
+    x = torch.as_tensor(sc["x0"].ravel(), device=dev)
+    v = torch.as_tensor(sc["v0"].ravel(), device=dev)
+    tot = {"newton_iters": 0, "pcg_iters": 0, "ws_iters": 0, "frames": 0, "converged": 0}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(frames or 1):
+        xn, vn = torch.empty_like(x), torch.empty_like(v)
+        bal.bal_frame_begin(ctx, x, v)
+        if newton:
+            bal.bal_frame_iterate(ctx, newton)
+        else:
+            bal.bal_frame_iterate(ctx, sc["params"]["max_newton"])
+        s = bal.bal_frame_finish(ctx, xn, vn, allow_unconverged=True)
+        for k in ("newton_iters", "pcg_iters", "ws_iters"):
+            tot[k] += s[k]
+        tot["frames"] += 1
+        tot["converged"] += int(s["converged"])
+        x, v = xn, vn
+    e1.record(st)
+    torch.cuda.synchronize()
+    tot["seconds"] = e0.elapsed_time(e1) / 1e3
+    return tot
+
+
+def main():
+    which = sys.argv[1] if len(sys.argv) > 1 else "c1"
+    k = int(sys.argv[2]) if len(sys.argv) > 2 else (10 if which == "c1" else 20)
+    sc = scenes.make_cubes(1) if which == "c1" else scenes.make_puffer_net(seed=4)
+    for name, fl in VARIANTS.items():
+        r = run(sc, fl, frames=k) if which == "c1" else run(sc, fl, newton=k)
+        print(json.dumps({"scene": which, "variant": name, **r}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,67 @@
+"""Long run: whole C4 frames through bal_step (device timing), written to profiles/c4_frames.json.
+
+    python tools/c4_frames.py [n_frames] [--chi X]
+
+Records per frame: seconds (CUDA events), Newton / PCG / warm-start iterations, max |A|, converged,
+per-phase ms.  bench.py reads `newton_per_frame` from it for its labelled s/frame projection."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2407_00046_b200 as bal  # noqa: E402
+import scenes  # noqa: E402
+
+
+def main():
+    nf = int(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else 1
+    kw = {}
+    if "--chi" in sys.argv:
+        kw["chi"] = float(sys.argv[sys.argv.index("--chi") + 1])
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join("profiles", "c4_frames.json")
+    sc = scenes.make_puffer_net(seed=4, **kw)
+    dev = torch.device("cuda:0")
+    ctx = bal.bal_init(sc)
+    st = torch.cuda.current_stream(dev)
+    x = torch.as_tensor(sc["x0"].ravel(), device=dev)
+    v = torch.as_tensor(sc["v0"].ravel(), device=dev)
+    frames = []
+    for f in range(nf):
+        xn, vn = torch.empty_like(x), torch.empty_like(v)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        bal.bal_frame_begin(ctx, x, v)
+        while not bal.bal_frame_iterate(ctx, 16):
+            s = bal.bal_frame_stats(ctx)
+            print(f"  frame {f}: newton {s['newton_iters']} pcg {s['pcg_iters']} t {s['ms_total'] / 1e3:.1f}s "
+                  f"rel_grad {s['last_rel_grad']:.3e}", flush=True)
+            if s["newton_iters"] >= sc["params"]["max_newton"]:
+                break
+        s = bal.bal_frame_finish(ctx, xn, vn, allow_unconverged=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        rec = {"frame": f, "seconds": e0.elapsed_time(e1) / 1e3, **{k: (float(v_) if isinstance(v_, float) else v_)
+                                                                      for k, v_ in s.items()}}
+        frames.append(rec)
+        print(json.dumps(rec), flush=True)
+        x, v = xn, vn
+    conv = [fr for fr in frames if fr["converged"]]
+    res = {"scene": "C4 puffer-net (scenes.make_puffer_net(seed=4" + "".join(f", {k}={v}" for k, v in kw.items())
+                    + "))", "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+           "gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+           "frames": frames,
+           "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in frames])),
+           "seconds_per_frame": float(np.mean([fr["seconds"] for fr in frames])),
+           "frames_converged": len(conv)}
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1)
+    print(json.dumps({k: v_ for k, v_ in res.items() if k != "frames"}))
+
+
+if __name__ == "__main__":
+    main()
