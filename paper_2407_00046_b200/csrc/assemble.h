@@ -46,6 +46,14 @@ struct StaticPattern {
   int* diag_pos = nullptr;   // [n]
   int* slot_ptr = nullptr;   // [nnzb+1]
   int* slot_code = nullptr;  // [16 T] tet*16 + a*4 + b
+  // symmetric copy for the SpMV (kernels.h Bsr): lower + diagonal slots in their own CSR
+  int nl = 0, nu = 0;
+  int* lpos = nullptr;       // [nnzb] position of a full slot in the lower storage, -1 for upper
+  int* l_row_ptr = nullptr;  // [n+1]
+  int* l_col = nullptr;      // [nl]
+  int* u_row_ptr = nullptr;  // [n+1] mirror index: row i, j > i
+  int* u_pos = nullptr;      // [nu] lower-storage position of (j, i)
+  int* u_col = nullptr;      // [nu] j
 };
 
 // Per-Newton-iteration contact/friction BSR built by sorting (row,col) keys.
@@ -55,14 +63,12 @@ struct ContactWork {
   DevBuf<unsigned char> tmp;
   DevBuf<int> row_ptr, col;
   DevBuf<double> val;
-  DevBuf<int> split, tpos, mflag;  // symmetric-SpMV mirror index (kernels.h Bsr)
-  bool sym = false;
   int nslots = 0;
   int nrows = 0;  // non-empty contact rows (= contact diagonal slots)
 };
 
 void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage, const double* mass,
-                   double inv_h2, const uint8_t* fixed, double* val);
+                   double inv_h2, const uint8_t* fixed, double* val, double* lval);
 int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* nodes, const uint8_t* fixed, int n,
                           const double* stage);
 void node_finalize(cudaStream_t st, int n, const double* x, const double* y, const double* mass, double inv_h2,

@@ -18,19 +18,20 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.row_ptr = lb_row_ptr.ptr;
     b.col = lb_col.ptr;
     b.val = lb_val.ptr;
-    if (lb_sym) {
-      b.split = lb_split.ptr;
-      b.tpos = lb_tpos.ptr;
-    }
+  } else if (sp_sym) {
+    b.nnzb = sp.nl;
+    b.row_ptr = sp.l_row_ptr;
+    b.col = sp.l_col;
+    b.val = lval.ptr;
+    b.m_row_ptr = sp.u_row_ptr;
+    b.m_pos = sp.u_pos;
+    b.m_col = sp.u_col;
+    b.nmirror = sp.nu;
   } else {
     b.nnzb = sp.nnzb;
     b.row_ptr = sp.row_ptr;
     b.col = sp.col;
     b.val = sval.ptr;
-    if (sp_sym) {
-      b.split = sp_split.ptr;
-      b.tpos = sp_tpos.ptr;
-    }
   }
   return b;
 }
@@ -42,10 +43,6 @@ bal::Bsr bal_ctx::contact_bsr() const {
   b.row_ptr = cw.row_ptr.ptr;
   b.col = cw.col.ptr;
   b.val = cw.val.ptr;
-  if (cw.sym) {
-    b.split = cw.split.ptr;
-    b.tpos = cw.tpos.ptr;
-  }
   return b;
 }
 
@@ -310,11 +307,46 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->sp.diag_pos = c->sp_diag_pos.ptr;
   c->sp.slot_ptr = c->sp_slot_ptr.ptr;
   c->sp.slot_code = c->sp_slot_code.ptr;
-  c->sp_split.reserve(N);
-  c->sp_tpos.reserve(nnzb);
-  c->mflag.reserve(1);
-  c->sp_sym = spmv_symmetric_enabled() &&
-              build_mirror(st, N, nnzb, c->sp.row_ptr, c->sp.col, c->sp_split.ptr, c->sp_tpos.ptr, c->mflag.ptr);
+  // symmetric copy for the SpMV: lower + diagonal slots in row order, and per row i the mirror
+  // index of its upper slots (j > i) -> lower-storage position of (j, i)
+  {
+    std::vector<int> lpos(nnzb, -1), lrow(N + 1, 0), lcol, urow(N + 1, 0), upos, ucol;
+    lcol.reserve((nnzb + N) / 2);
+    for (int i = 0; i < N; ++i) {
+      for (int s2 = row_ptr[i]; s2 < row_ptr[i + 1]; ++s2)
+        if (col[s2] <= i) {
+          lpos[s2] = (int)lcol.size();
+          lcol.push_back(col[s2]);
+        }
+      lrow[i + 1] = (int)lcol.size();
+    }
+    for (int i = 0; i < N; ++i) {
+      for (int s2 = row_ptr[i]; s2 < row_ptr[i + 1]; ++s2)
+        if (col[s2] > i) {
+          const int j = col[s2];
+          upos.push_back(lpos[find_slot(j, i)]);
+          ucol.push_back(j);
+        }
+      urow[i + 1] = (int)ucol.size();
+    }
+    c->sp.nl = (int)lcol.size();
+    c->sp.nu = (int)ucol.size();
+    c->sp_lpos.upload(lpos.data(), lpos.size(), st);
+    c->sp_lrow.upload(lrow.data(), lrow.size(), st);
+    c->sp_lcol.upload(lcol.data(), std::max<size_t>(lcol.size(), 1), st);
+    c->sp_urow.upload(urow.data(), urow.size(), st);
+    c->sp_upos.upload(upos.data(), std::max<size_t>(upos.size(), 1), st);
+    c->sp_ucol.upload(ucol.data(), std::max<size_t>(ucol.size(), 1), st);
+    c->sp.lpos = c->sp_lpos.ptr;
+    c->sp.l_row_ptr = c->sp_lrow.ptr;
+    c->sp.l_col = c->sp_lcol.ptr;
+    c->sp.u_row_ptr = c->sp_urow.ptr;
+    c->sp.u_pos = c->sp_upos.ptr;
+    c->sp.u_col = c->sp_ucol.ptr;
+    c->sp_sym = spmv_symmetric_enabled();
+    if (c->sp_sym) c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1));
+    spmv_init_grids();
+  }
   c->sval.reserve(9 * (size_t)nnzb);
   c->stage_e.reserve(90 * (size_t)std::max(T, 1));
   c->grad_e.reserve(12 * (size_t)std::max(T, 1));
@@ -367,7 +399,8 @@ void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
                       c->grad_c.ptr + 12 * (size_t)nc, c->lbar_c.ptr + nc, c->nodes_c.ptr + 4 * (size_t)nc);
   }
   const double inv_h2 = 1.0 / (c->prm.h * c->prm.h);
-  gather_static(st, c->sp, c->stage_e.ptr, c->mass.ptr, inv_h2, c->fixed.ptr, c->sval.ptr);
+  gather_static(st, c->sp, c->stage_e.ptr, c->mass.ptr, inv_h2, c->fixed.ptr, c->sval.ptr,
+                c->sp_sym ? c->lval.ptr : nullptr);
   build_contact_pattern(st, c->cw, ns, c->nodes_c.ptr, c->fixed.ptr, N, c->stage_c.ptr);
   if (ns == 0) c->cw.nslots = 0;
   node_finalize(st, N, x, y, c->mass.ptr, inv_h2, c->fixed.ptr, c->sp, c->grad_e.ptr, c->lbar_e.ptr, c->sval.ptr,
@@ -513,12 +546,7 @@ bal_status bal_load_bsr(bal_ctx* c, const bal_bsr_host* b) {
     c->lb_val.upload(b->val, 9 * (size_t)b->nnzb, st);
     c->lb_nnzb = b->nnzb;
     c->loaded_bsr = true;
-    c->lb_split.reserve(c->N);
-    c->lb_tpos.reserve(std::max(b->nnzb, 1));
-    c->mflag.reserve(1);
-    c->lb_sym = spmv_symmetric_enabled() && b->nnzb > 0 &&
-                build_mirror(st, c->N, b->nnzb, c->lb_row_ptr.ptr, c->lb_col.ptr, c->lb_split.ptr, c->lb_tpos.ptr,
-                             c->mflag.ptr);
+
     // diagonal inverse from the loaded blocks (host: test path only)
     std::vector<double> dinv(6 * (size_t)c->N, 0.0);
     for (int i = 0; i < c->N; ++i) {

@@ -33,8 +33,9 @@ struct bal_ctx {
   bal::DevBuf<int> sp_row_ptr, sp_col, sp_slot_row, sp_diag_pos, sp_slot_ptr, sp_slot_code;
   bal::StaticPattern sp;
   bal::DevBuf<double> sval;
-  bal::DevBuf<int> sp_split, sp_tpos, lb_split, lb_tpos, mflag;  // symmetric-SpMV mirror index
-  bool sp_sym = false, lb_sym = false;
+  bal::DevBuf<int> sp_lpos, sp_lrow, sp_lcol, sp_urow, sp_upos, sp_ucol;  // symmetric SpMV copy
+  bal::DevBuf<double> lval;
+  bool sp_sym = false;
   // ---- elastic stencils
   bal::DevBuf<double> stage_e, grad_e, lbar_e;
   // ---- contact + friction stencils (friction appended after contact)
@@ -79,16 +80,13 @@ struct bal_ctx {
   // bytes the SpMV kernel as configured must move at minimum: symmetric mode streams lower +
   // diagonal blocks (76 B with the column) and reads column + mirror index (8 B) per upper slot;
   // full mode streams every stored block
-  static double part_bytes(double n, double nnzb, double diag, bool sym) {
-    if (nnzb <= 0) return 0.0;
-    if (!sym) return 76.0 * nnzb + 4.0 * (n + 1);
-    const double lo = 0.5 * (nnzb + diag), up = 0.5 * (nnzb - diag);
-    return 76.0 * lo + 8.0 * up + 8.0 * n + 4.0;
-  }
   double spmv_moved_bytes() const {
     const double n = N;
-    if (loaded_bsr) return part_bytes(n, lb_nnzb, n, lb_sym) + 48.0 * n;
-    return part_bytes(n, sp.nnzb, n, sp_sym) + part_bytes(n, cw.nslots, cw.nrows, cw.sym) + 48.0 * n;
+    const double cc = loaded_bsr ? 0 : cw.nslots;
+    const double contact = cc > 0 ? 76.0 * cc + 4.0 * (n + 1) : 0.0;
+    if (loaded_bsr) return 76.0 * lb_nnzb + 4.0 * (n + 1) + 48.0 * n;
+    const double stat = sp_sym ? 76.0 * sp.nl + 8.0 * sp.nu + 8.0 * (n + 1) : 76.0 * sp.nnzb + 4.0 * (n + 1);
+    return stat + contact + 48.0 * n;
   }
 
   // ---- time-step work (bal_step.cu), allocated on first use

@@ -61,7 +61,8 @@ BAL_D const double* code_block(const double* __restrict__ stage, int code, bool&
 __global__ void k_gather_static(int nnzb, const int* __restrict__ slot_row, const int* __restrict__ col,
                                 const int* __restrict__ slot_ptr, const int* __restrict__ slot_code,
                                 const double* __restrict__ stage, const double* __restrict__ mass, double inv_h2,
-                                const uint8_t* __restrict__ fixed, double* __restrict__ val) {
+                                const uint8_t* __restrict__ fixed, double* __restrict__ val,
+                                const int* __restrict__ lpos, double* __restrict__ lval) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nnzb) return;
   const int i = slot_row[s], j = col[s];
@@ -79,6 +80,14 @@ __global__ void k_gather_static(int nnzb, const int* __restrict__ slot_row, cons
   double* o = val + 9 * (size_t)s;
 #pragma unroll
   for (int t = 0; t < 9; ++t) o[t] = acc[t];
+  if (lval) {
+    const int lp = lpos[s];
+    if (lp >= 0) {
+      double* ol = lval + 9 * (size_t)lp;
+#pragma unroll
+      for (int t = 0; t < 9; ++t) ol[t] = acc[t];
+    }
+  }
 }
 
 // contact slots: contributions are the sorted entries [start[s], start[s+1])
@@ -232,9 +241,9 @@ __global__ void k_node_finalize(int n, const double* __restrict__ x, const doubl
 
 // ---------------------------------------------------------------------------- host side
 void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage, const double* mass,
-                   double inv_h2, const uint8_t* fixed, double* val) {
+                   double inv_h2, const uint8_t* fixed, double* val, double* lval) {
   k_gather_static<<<ceil_div(sp.nnzb, 256), 256, 0, st>>>(sp.nnzb, sp.slot_row, sp.col, sp.slot_ptr, sp.slot_code,
-                                                           stage, mass, inv_h2, fixed, val);
+                                                           stage, mass, inv_h2, fixed, val, sp.lpos, lval);
   CK(cudaGetLastError());
 }
 
@@ -284,13 +293,6 @@ int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* no
   k_count_rows<<<ceil_div(n, 256), 256, 0, st>>>(n, w.row_ptr.ptr, w.nvalid.ptr);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&w.nrows, w.nvalid.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
-  w.sym = false;
-  if (nslots > 0 && spmv_symmetric_enabled()) {
-    w.split.reserve(n);
-    w.tpos.reserve(nslots);
-    w.mflag.reserve(1);
-    w.sym = build_mirror(st, n, nslots, w.row_ptr.ptr, w.col.ptr, w.split.ptr, w.tpos.ptr, w.mflag.ptr);
-  }
   return nslots;
 }
 

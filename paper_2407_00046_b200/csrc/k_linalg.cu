@@ -20,84 +20,169 @@
 namespace bal {
 
 constexpr int kSL = 16;        // lanes per block row
-constexpr int kSpmvThreads = 256;
-constexpr int kSpmvBlocks = 16 * kSMs;
-
-// Lane mapping: a 16-lane half-warp owns one block row; its lanes 0..11 form 4 block slots x 3
-// component rows (q = lane/3, r = lane%3), lanes 12..15 idle.  Per pass the half-warp consumes 4
-// blocks of the row: lane (q, r) multiplies row r of block q (or column r when the block is the
-// mirror A_ji of an upper slot, i.e. (A_ji)^T) with the 3 components of v at the block's column
-// and accumulates one scalar y_r.  A row's result is two shuffles away (strides 6 and 3).  Each
-// lane's three value loads read 24 contiguous bytes; the 12 lanes read a block's 72 bytes whole.
-constexpr int kLanesPerRow = 12;
-constexpr int kBlocksPerPass = kLanesPerRow / 3;
-
-template <bool MASK>
-BAL_D double row_accum(const Bsr& A, int row, int q, int r, const double* __restrict__ v, const int* __restrict__ grp,
-                       int gr) {
-  const int beg = __ldg(A.row_ptr + row), end = __ldg(A.row_ptr + row + 1);
-  const int split = A.tpos ? __ldg(A.split + row) : end;
-  double acc = 0.0;
-#pragma unroll 2
-  for (int s = beg + q; s < end; s += kBlocksPerPass) {
-    const bool up = s >= split;
-    const int blk = up ? __ldg(A.tpos + s) : s;
-    const int col = __ldg(A.col + s);
-    double x0 = __ldg(v + 3 * (size_t)col), x1 = __ldg(v + 3 * (size_t)col + 1),
-           x2 = __ldg(v + 3 * (size_t)col + 2);
-    if (MASK && __ldg(grp + col) != gr) x0 = x1 = x2 = 0.0;
-    const double* __restrict__ a = A.val + 9 * (size_t)blk;
-    double a0, a1, a2;
-    if (up) {  // column r of the mirror block A_ji (read through L2; an earlier row streamed it)
-      a0 = __ldg(a + r);
-      a1 = __ldg(a + 3 + r);
-      a2 = __ldg(a + 6 + r);
-    } else {  // row r of this row's own block, streamed once: evict-first
-      a0 = __ldcs(a + 3 * r);
-      a1 = __ldcs(a + 3 * r + 1);
-      a2 = __ldcs(a + 3 * r + 2);
-    }
-    acc = fma(a0, x0, acc);
-    acc = fma(a1, x1, acc);
-    acc = fma(a2, x2, acc);
+constexpr int kSpmvThreads = 128;
+constexpr int kSpmvMinBlocks = 16;  // 12 x 128 threads resident per SM: independent tile pipelines
+constexpr int kTileRows = 16;  // block rows per SpMV tile
+// persistent grid: exactly the resident CTAs, so the grid-stride sweep visits rows in increasing
+// order wave by wave (the mirror-block L2 reuse above depends on it)
+template <bool DOT, bool MASK>
+__global__ void k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v,
+                       double* __restrict__ y, double* partials, unsigned* counter, PcgScal* sc, const GrpScal* gs);
+template <bool DOT, bool MASK>
+static int spmv_grid(int n) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<DOT, MASK>, kSpmvThreads, 0));
+    per_sm = std::max(per_sm, 1);
   }
-  return acc;
+  return std::max(1, std::min(per_sm * kSMs, ceil_div((long long)n, kTileRows)));
 }
 
+// Tiled, flattened SpMV.  A CTA owns a tile of kTileRows consecutive block rows and walks the
+// tile's blocks from up to three lists -- the stored static blocks (lower + diagonal in symmetric
+// mode, all blocks otherwise), the mirror entries of the static part (transposes of stored blocks
+// A_ji, j > i) and the stored contact blocks -- as ONE flat sequence, so the dependent loads
+// (row pointers -> column / mirror index -> values and v) cost three latency levels per tile, not
+// per row.  Stage 1: row pointers of the tile (and groups when masked) to shared memory.  Stage 2:
+// per block, its column and value-block index.  Stage 3: per (block, component row r) item, the
+// 3-term product of row r (stored) or column r (mirror) with v at the block's column -> shared
+// memory.  Stage 4: thread (row, r) sums its blocks in fixed order (list 0, 1, 2; ascending) --
+// bitwise deterministic, atomic-free.  Stored blocks are streamed with L2 evict_first, mirror
+// blocks read with evict_last (the earlier row pulls the block, its own row streams it); the grid
+// is persistent (the resident CTAs) and sweeps tiles in increasing order, so both reads of a
+// block fall within one L2 lifetime.
+constexpr int kTileCap = 320;  // blocks staged per chunk
+
+BAL_D unsigned long long policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+BAL_D unsigned long long policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+BAL_D double ld_hint(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+struct SpmvSmem {
+  int rp[3][kTileRows + 1];
+  int rgrp[kTileRows];
+  int bcol[kTileCap];
+  int bblk[kTileCap];
+  unsigned char blist[kTileCap];
+  double contrib[kTileCap][3];
+};
+
 template <bool DOT, bool MASK>
-__global__ void __launch_bounds__(kSpmvThreads)
+__global__ void __launch_bounds__(kSpmvThreads, kSpmvMinBlocks)
 k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, double* __restrict__ y,
        double* partials, unsigned* counter, PcgScal* sc, const GrpScal* gs) {
   if (DOT && sc->done) return;
+  __shared__ SpmvSmem sm;
   const int n = S.n;
-  const int lane = threadIdx.x & (kSL - 1);
-  const int q = lane / 3, r = lane - 3 * (lane / 3);
-  const bool active_lane = lane < kLanesPerRow;
-  const int sub_in_warp = (threadIdx.x & 31) / kSL;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  constexpr int kRowsPerWarp = 32 / kSL;
+  const int tid = threadIdx.x;
+  const unsigned long long pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  const int ntiles = (n + kTileRows - 1) / kTileRows;
+  const int* crp = C.nnzb > 0 ? C.row_ptr : nullptr;
   double dacc = 0.0;
-  for (int base = gwarp * kRowsPerWarp; base < n; base += nwarps * kRowsPerWarp) {
-    const int row = base + sub_in_warp;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int r0 = tile * kTileRows;
+    const int R = min(kTileRows, n - r0);
+    // ---- stage 1: row pointers (3 lists) and row groups
+    for (int t = tid; t < 3 * (kTileRows + 1); t += blockDim.x) {
+      const int L = t / (kTileRows + 1), k = t - L * (kTileRows + 1);
+      const int* rp = L == 0 ? S.row_ptr : (L == 1 ? S.m_row_ptr : crp);
+      sm.rp[L][k] = (rp && k <= R) ? __ldg(rp + r0 + k) : 0;
+    }
+    if (MASK && tid < R) {
+      const int g = grp[r0 + tid];
+      sm.rgrp[tid] = (g >= 0 && gs->active[g]) ? g : -1;
+    }
+    __syncthreads();
+    const int n0 = sm.rp[0][R] - sm.rp[0][0];
+    const int n1 = S.m_row_ptr ? sm.rp[1][R] - sm.rp[1][0] : 0;
+    const int n2 = crp ? sm.rp[2][R] - sm.rp[2][0] : 0;
+    const int nt = n0 + n1 + n2;
+    // thread (row, r) accumulator, persistent across chunks
+    const int my_row = tid / 3, my_r = tid - 3 * (tid / 3);
+    const bool reducer = tid < 3 * R;
     double acc = 0.0;
-    bool valid = row < n;
-    int gr = 0;
-    if (MASK && valid) {
-      gr = grp[row];
-      valid = gr >= 0 && gs->active[gr];
+    for (int c0 = 0; c0 < nt; c0 += kTileCap) {
+      const int nb = min(kTileCap, nt - c0);
+      // ---- stage 2: column and value-block index of every block of the chunk
+      for (int b = tid; b < nb; b += blockDim.x) {
+        const int g = c0 + b;
+        int col, blk, L;
+        if (g < n0) {
+          blk = sm.rp[0][0] + g;
+          col = __ldg(S.col + blk);
+          L = 0;
+        } else if (g < n0 + n1) {
+          const int m = sm.rp[1][0] + (g - n0);
+          blk = __ldg(S.m_pos + m);
+          col = __ldg(S.m_col + m);
+          L = 1;
+        } else {
+          blk = sm.rp[2][0] + (g - n0 - n1);
+          col = __ldg(C.col + blk);
+          L = 2;
+        }
+        sm.bcol[b] = col;
+        sm.bblk[b] = blk;
+        sm.blist[b] = (unsigned char)L;
+      }
+      __syncthreads();
+      // ---- stage 3: item (b, r): row r (stored) / column r (mirror) of the block times v[col]
+      const int ni = 3 * nb;
+#pragma unroll 4
+      for (int k = tid; k < ni; k += blockDim.x) {
+        const int b = k / 3, r = k - 3 * (k / 3);
+        const int L = sm.blist[b];
+        const int col = sm.bcol[b];
+        const bool tr = L == 1;
+        const double* __restrict__ pv = (L == 2 ? C.val : S.val) + 9 * (size_t)sm.bblk[b] + (tr ? r : 3 * r);
+        const int st = tr ? 3 : 1;
+        const unsigned long long pol = tr ? pol_last : pol_first;
+        const double* __restrict__ vc = v + 3 * (size_t)col;
+        const double a0 = ld_hint(pv, pol), a1 = ld_hint(pv + st, pol), a2 = ld_hint(pv + 2 * st, pol);
+        const double x0 = __ldg(vc), x1 = __ldg(vc + 1), x2 = __ldg(vc + 2);
+        sm.contrib[b][r] = fma(a2, x2, fma(a1, x1, a0 * x0));
+      }
+      __syncthreads();
+      // ---- stage 4: fixed-order row sums (list 0, then 1, then 2; ascending)
+      if (reducer) {
+        const int gr = MASK ? sm.rgrp[my_row] : 0;
+        int off = 0;
+#pragma unroll
+        for (int L = 0; L < 3; ++L) {
+          const int nL = L == 0 ? n0 : (L == 1 ? n1 : n2);
+          if (nL > 0) {
+            const int lo = max(off + sm.rp[L][my_row] - sm.rp[L][0], c0);
+            const int hi = min(off + sm.rp[L][my_row + 1] - sm.rp[L][0], c0 + nb);
+            for (int g = lo; g < hi; ++g) {
+              if (MASK && __ldg(grp + sm.bcol[g - c0]) != gr) continue;
+              acc += sm.contrib[g - c0][my_r];
+            }
+          }
+          off += nL;
+        }
+      }
+      __syncthreads();
     }
-    if (valid && active_lane) {
-      acc = row_accum<MASK>(S, row, q, r, v, grp, gr);
-      if (C.nnzb > 0) acc += row_accum<MASK>(C, row, q, r, v, grp, gr);
+    if (reducer) {
+      const int row = r0 + my_row;
+      const bool valid = !MASK || sm.rgrp[my_row] >= 0;
+      if (valid) {
+        y[3 * (size_t)row + my_r] = acc;
+        if (DOT) dacc += v[3 * (size_t)row + my_r] * acc;
+      }
     }
-    // lanes r, r+3, r+6, r+9 of the half-warp hold the partial sums of component r
-    acc += __shfl_down_sync(0xffffffffu, acc, 6, kSL);
-    acc += __shfl_down_sync(0xffffffffu, acc, 3, kSL);
-    if (valid && lane < 3) {
-      y[3 * (size_t)row + lane] = acc;
-      if (DOT) dacc += v[3 * (size_t)row + lane] * acc;
-    }
+    __syncthreads();  // sm.rp / rgrp are rewritten by the next tile
   }
   if (DOT) {
     __shared__ double sh[kSpmvThreads / 32];
@@ -123,61 +208,31 @@ k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, 
   }
 }
 
+void spmv_init_grids() {  // occupancy queries outside any stream capture (called by bal_init)
+  (void)spmv_grid<false, false>(1);
+  (void)spmv_grid<true, false>(1);
+  (void)spmv_grid<false, true>(1);
+}
+
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y) {
   if (S.n <= 0) return;
-  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  const int blocks = spmv_grid<false, false>(S.n);
   k_spmv<false, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, nullptr, nullptr, nullptr, nullptr);
   CK(cudaGetLastError());
 }
 
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* partials,
                      unsigned* counter, PcgScal* sc) {
-  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  const int blocks = spmv_grid<true, false>(S.n);
   k_spmv<true, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, partials, counter, sc, nullptr);
   CK(cudaGetLastError());
 }
 
 void launch_spmv_masked(cudaStream_t st, const Bsr& S, const Bsr& C, const int* grp, const double* v, double* y,
                         const GrpScal* gs) {
-  const int blocks = std::min(kSpmvBlocks, ceil_div((long long)S.n * kSL, kSpmvThreads));
+  const int blocks = spmv_grid<false, true>(S.n);
   k_spmv<false, true><<<blocks, kSpmvThreads, 0, st>>>(S, C, grp, v, y, nullptr, nullptr, nullptr, gs);
   CK(cudaGetLastError());
-}
-
-// mirror index: split[i] = first slot of row i with col > i; tpos[s] = slot of (col[s], i)
-__global__ void k_bsr_mirror(int n, const int* __restrict__ row_ptr, const int* __restrict__ col,
-                             int* __restrict__ split, int* __restrict__ tpos, int* bad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int beg = row_ptr[i], end = row_ptr[i + 1];
-  int sp = end;
-  for (int s = beg; s < end; ++s) {
-    const int j = col[s];
-    if (s > beg && col[s - 1] >= j) atomicExch(bad, 1);  // rows must be strictly column-sorted
-    if (j > i && sp == end) sp = s;
-    int lo = row_ptr[j], hi = row_ptr[j + 1];
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (col[mid] < i) lo = mid + 1;
-      else hi = mid;
-    }
-    if (lo < row_ptr[j + 1] && col[lo] == i) tpos[s] = lo;
-    else atomicExch(bad, 1);
-  }
-  split[i] = sp;
-}
-
-bool build_mirror(cudaStream_t st, int n, int nnzb, const int* row_ptr, const int* col, int* split, int* tpos,
-                  int* flag_dev) {
-  if (n <= 0) return false;
-  CK(cudaMemsetAsync(flag_dev, 0, sizeof(int), st));
-  k_bsr_mirror<<<ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, col, split, tpos, flag_dev);
-  CK(cudaGetLastError());
-  int bad = 1;
-  CK(cudaMemcpyAsync(&bad, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  (void)nnzb;
-  return bad == 0;
 }
 
 // ---------------------------------------------------------------------------------- vectors

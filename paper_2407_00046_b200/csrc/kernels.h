@@ -28,25 +28,24 @@ void launch_friction_energy(cudaStream_t st, int n, const double* x, const doubl
 // ---- sparse system (k_linalg.cu)
 struct Bsr {
   int n = 0;             // block rows
-  int nnzb = 0;
+  int nnzb = 0;          // stored blocks
   const int* row_ptr = nullptr;
   const int* col = nullptr;
   const double* val = nullptr;
-  // symmetric mode (both set): row i streams only its slots [row_ptr[i], split[i]) (lower blocks +
-  // diagonal) and applies each upper slot s in [split[i], row_ptr[i+1]) as the transpose of its
-  // mirror block val[tpos[s]] = A_ji -- every off-diagonal block leaves HBM once (the
-  // paper's D + L + L^T storage) and the mirror read hits L2.  Null = stream every stored block.
-  const int* split = nullptr;  // [n]
-  const int* tpos = nullptr;   // [nnzb]
+  // Symmetric storage (the paper's D + L + L^T): when m_row_ptr is set, the stored part
+  // holds only the lower blocks and the diagonal (col <= row), and row i additionally applies, for
+  // every j > i in m_col[m_row_ptr[i] .. m_row_ptr[i+1]), the transpose of the stored block
+  // val[m_pos[.]] = A_ji.  Every off-diagonal block leaves HBM once; the mirror read is served by
+  // L2 (an earlier row pulls the block, its own row streams it).  Null = every block is stored.
+  const int* m_row_ptr = nullptr;  // [n+1]
+  const int* m_pos = nullptr;      // [m_row_ptr[n]]
+  const int* m_col = nullptr;      // [m_row_ptr[n]]
+  int nmirror = 0;
 };
-// mirror index of a pattern-symmetric BSR with column-sorted rows: split[i], tpos[s]; returns
-// false (no symmetric mode) when a slot has no mirror
 inline bool spmv_symmetric_enabled() {
-  static const bool full = getenv("BAL_SPMV_FULL") != nullptr;  // A/B switch: stream both triangles
+  static const bool full = getenv("BAL_SPMV_FULL") != nullptr;  // A/B switch: full static BSR in the SpMV
   return !full;
 }
-bool build_mirror(cudaStream_t st, int n, int nnzb, const int* row_ptr, const int* col, int* split, int* tpos,
-                  int* flag_dev);
 
 // PCG scalars living in device memory (single group)
 struct PcgScal {
@@ -63,6 +62,7 @@ struct GrpScal {
   double tol;
 };
 
+void spmv_init_grids();
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y);
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,
                      double* partials, unsigned* counter, PcgScal* sc);
