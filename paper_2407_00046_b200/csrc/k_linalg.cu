@@ -21,7 +21,7 @@ namespace bal {
 
 constexpr int kSL = 16;        // lanes per block row
 constexpr int kSpmvThreads = 128;
-constexpr int kSpmvMinBlocks = 16;  // 12 x 128 threads resident per SM: independent tile pipelines
+constexpr int kSpmvMinBlocks = 16;  // 16 x 128 threads resident per SM: independent tile pipelines
 constexpr int kTileRows = 16;  // block rows per SpMV tile
 // persistent grid: exactly the resident CTAs, so the grid-stride sweep visits rows in increasing
 // order wave by wave (the mirror-block L2 reuse above depends on it)

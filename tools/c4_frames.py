@@ -24,6 +24,8 @@ def main():
         kw["chi"] = float(sys.argv[sys.argv.index("--chi") + 1])
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join("profiles", "c4_frames.json")
     sc = scenes.make_puffer_net(seed=4, **kw)
+    if "--max-newton" in sys.argv:
+        sc["params"]["max_newton"] = int(sys.argv[sys.argv.index("--max-newton") + 1])
     dev = torch.device("cuda:0")
     ctx = bal.bal_init(sc)
     st = torch.cuda.current_stream(dev)
@@ -56,7 +58,8 @@ def main():
            "frames": frames,
            "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in frames])),
            "seconds_per_frame": float(np.mean([fr["seconds"] for fr in frames])),
-           "frames_converged": len(conv)}
+           "frames_converged": len(conv), "max_newton": int(sc["params"]["max_newton"]),
+           "note": "newton_per_frame counts the Newton cap for frames that did not converge"}
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
