@@ -14,6 +14,8 @@
 // skipped), per-group scalars in one GrpScal, group-wise deterministic warp-match reductions.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -393,6 +395,97 @@ __global__ void k_pcg_pupdate(int n3, const double* __restrict__ z, double* __re
   if (sc->done) return;
   const double beta = sc->beta;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n3; j += gridDim.x * blockDim.x) p[j] = z[j] + beta * p[j];
+}
+
+// Fused update + p-update (one kernel per PCG iteration after the SpMV): x += alpha p, r -= alpha q,
+// z = D^{-1} r kept in registers (never written), block partials of r.z and r.r, a grid-wide
+// barrier (cooperative launch: the grid is co-resident), every CTA re-reduces the partials in the
+// same fixed order (identical beta everywhere, deterministic), CTA 0 updates the scalars and the
+// App. B stop test, then p = z + beta p.  Saves the z round trip and one launch per iteration.
+constexpr int kFuseMax = 8;  // nodes per thread held in registers
+__global__ void __launch_bounds__(kVecThreads)
+k_pcg_update_fused(int n, const double* __restrict__ dinv, double* __restrict__ p, const double* __restrict__ q,
+                   double* __restrict__ x, double* __restrict__ r, double* partials, PcgScal* sc, double* hist) {
+  if (sc->done) return;  // read by every CTA before CTA 0 can write it (after the barrier)
+  const double alpha = sc->alpha, rz_old = sc->rz;
+  const int T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+  double z[kFuseMax][3];
+  double loc0 = 0.0, loc1 = 0.0;
+#pragma unroll
+  for (int u = 0; u < kFuseMax; ++u) {
+    const int i = t + u * T;
+    z[u][0] = z[u][1] = z[u][2] = 0.0;
+    if (i < n) {
+      double rr[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t j = 3 * (size_t)i + c;
+        x[j] = x[j] + alpha * p[j];
+        rr[c] = r[j] - alpha * q[j];
+        r[j] = rr[c];
+      }
+      dinv_apply(dinv, i, rr[0], rr[1], rr[2], z[u][0], z[u][1], z[u][2]);
+      loc0 += rr[0] * z[u][0] + rr[1] * z[u][1] + rr[2] * z[u][2];
+      loc1 += rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+    }
+  }
+  __shared__ double sh[kVecThreads / 32];
+  const double b0 = block_sum<kVecThreads>(loc0, sh);
+  const double b1 = block_sum<kVecThreads>(loc1, sh);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = b0;
+    partials[2 * blockIdx.x + 1] = b1;
+  }
+  cooperative_groups::this_grid().sync();
+  double t0 = 0.0, t1 = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    t0 += partials[2 * b];
+    t1 += partials[2 * b + 1];
+  }
+  const double rz = block_sum<kVecThreads>(t0, sh);
+  const double rr2 = block_sum<kVecThreads>(t1, sh);
+  const double beta = (rz_old != 0.0) ? rz / rz_old : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->dec += 0.5 * alpha * rz_old;
+    sc->beta = beta;
+    sc->rz = rz;
+    sc->rr = rr2;
+    const int k = sc->k + 1;
+    sc->k = k;
+    hist[k] = sqrt(rr2);
+    hist[sc->hcap + k] = sc->dec;
+    pcg_stop_check(sc, hist);
+  }
+#pragma unroll
+  for (int u = 0; u < kFuseMax; ++u) {
+    const int i = t + u * T;
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const size_t j = 3 * (size_t)i + c;
+        p[j] = z[u][c] + beta * p[j];
+      }
+    }
+  }
+}
+
+// grid for the fused update, 0 when it cannot hold n nodes (caller falls back to update + pupdate)
+int pcg_fused_grid(int n) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    const bool off = getenv("BAL_PCG_UNFUSED") != nullptr;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_update_fused, kVecThreads, 0));
+    if (off) per_sm = 0;
+  }
+  const long long cap = (long long)per_sm * kSMs * kVecThreads * kFuseMax;
+  if (per_sm <= 0 || n > cap) return 0;
+  return std::min(per_sm * kSMs, std::max(1, ceil_div((long long)n, (long long)kVecThreads * kFuseMax)));
+}
+
+void launch_pcg_update_fused(cudaStream_t st, int grid, int n, const double* dinv, double* p, const double* q,
+                             double* x, double* r, double* partials, PcgScal* sc, double* hist) {
+  void* args[] = {&n, &dinv, &p, &q, &x, &r, &partials, &sc, &hist};
+  CK(cudaLaunchCooperativeKernel((const void*)k_pcg_update_fused, dim3(grid), dim3(kVecThreads), args, 0, st));
 }
 
 void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc) {

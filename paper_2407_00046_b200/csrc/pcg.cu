@@ -65,6 +65,7 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
   cudaStream_t st = c->cap_stream;
   const int N = c->N;
   cudaEvent_t* ev = c->ev + set * (2 * kBatch + 1);
+  const int fg = pcg_fused_grid(N);  // occupancy query before the capture starts
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int it = 0; it < kBatch; ++it) {
@@ -73,9 +74,14 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
     CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
     launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
     CK(cudaEventRecordWithFlags(ev[2 * it + 1], st, cudaEventRecordExternal));
-    launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
-                      c->counter.ptr, c->scal.ptr, c->hist.ptr);
-    launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
+    if (fg > 0) {
+      launch_pcg_update_fused(st, fg, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->partials.ptr,
+                              c->scal.ptr, c->hist.ptr);
+    } else {
+      launch_pcg_update(st, N, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr, c->pr.ptr, c->pz.ptr, c->partials.ptr,
+                        c->counter.ptr, c->scal.ptr, c->hist.ptr);
+      launch_pcg_pupdate(st, N, c->pz.ptr, c->pp.ptr, c->scal.ptr);
+    }
   }
   CK(cudaMemcpyAsync(c->h_scal + 1 + set, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecordWithFlags(ev[2 * kBatch], st, cudaEventRecordExternal));
@@ -96,7 +102,8 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
   int k_prev = c->h_scal->k;
   CK(cudaGraphLaunch(ge[0], st));
   CK(cudaGraphLaunch(ge[1], st));
-  c->launches += 6 * kBatch;
+  const int per_iter = pcg_fused_grid(c->N) > 0 ? 2 : 3;
+  c->launches += 2 * per_iter * kBatch;
   int cur = 0;
   while (true) {
     cudaEvent_t* ev = c->ev + cur * (2 * kBatch + 1);
@@ -119,7 +126,7 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
       fprintf(stderr, "[bal-pcg] k=%d rr=%.3e bnorm=%.3e alpha=%.3e beta=%.3e\n", hs.k, std::sqrt(hs.rr), hs.bnorm,
               hs.alpha, hs.beta);
     CK(cudaGraphLaunch(ge[cur], st));  // re-queue this set behind the other in-flight batch
-    c->launches += 3 * kBatch;
+    c->launches += per_iter * kBatch;
     cur ^= 1;
   }
   CK(cudaStreamSynchronize(st));
