@@ -121,3 +121,78 @@ def test_c4_pcg_fixed_iterations(c4):
     st = la.pcg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
     assert s["iters"] == k == st.k
     assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
+
+
+@pytest.fixture(scope="module")
+def c4_contact():
+    """C4 with one free ring translated (as a rigid body) until its closest feature pair to a
+    neighbouring ring is 0.4 mm apart: a few hundred ring-ring constraints below dhat, found by the
+    oracle's brute-force broad phase on the surface primitives of a 12 cm box around them."""
+    import types
+
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+
+    from oracle import contact as cm
+    sc = scenes.make_puffer_net(seed=4)
+    m = precompute(sc)
+    N = len(sc["x0"])
+    x = sc["x0"].copy()
+    e = m.tets[:, [0, 1, 1, 2, 2, 3]].reshape(-1, 2)
+    _nc, lab = connected_components(sp.coo_matrix((np.ones(len(e)), (e[:, 0], e[:, 1])), shape=(N, N)),
+                                    directed=False)
+    net = np.zeros(N, bool)
+    net[np.unique(m.tets[sc["tet_material"] == 1])] = True
+    free_net = np.flatnonzero(net & ~m.fixed)
+    c = x[free_net[len(free_net) // 2]]
+    inside = np.all(np.abs(x - c) < 0.06, axis=1)
+    sub = types.SimpleNamespace(surf_verts=m.surf_verts[inside[m.surf_verts]], tris=m.tris[inside[m.tris].all(1)],
+                                edges=m.edges[inside[m.edges].all(1)], fixed=m.fixed)
+    dhat = sc["params"]["dhat"]
+    pt, ee = cm.candidates(sub, x, x, 8e-3)
+    keys8, d8 = cm.constraint_set(x, pt, ee, 8e-3)
+    k = keys8[np.argmin(d8)][None]
+    body = lab == lab[k[0, 1]]
+    for _ in range(3):  # Newton on the rigid translation of `body` along grad d
+        d0 = cm.key_distance(x, k)[0]
+        g = np.zeros(3)
+        for a in range(3):
+            x3 = x.copy()
+            x3[body, a] += 1e-6
+            g[a] = (cm.key_distance(x3, k)[0] - d0) / 1e-6
+        x[body] -= (d0 - 4e-4) * g / (g @ g)
+    keys, d = cm.constraint_set(x, pt, ee, dhat)
+    assert len(keys) > 50 and d.min() > 3e-4
+    return sc, m, x, keys, d
+
+
+def test_c4_contact_stencils_and_spmv_with_contacts(c4_contact):
+    from oracle import contact as cm
+    sc, m, x, keys, d = c4_contact
+    dhat = sc["params"]["dhat"]
+    sigma = 2.3e4
+    ctx = bal.bal_init(sc)
+    out = bal.bal_assemble(ctx, _t(x), active_keys=keys, sigma=sigma)
+    n = len(keys)
+    cs = cm.contact_stencils(x, keys, np.ones(n), np.zeros(n), np.zeros(n), np.zeros(n), sigma, dhat)
+    nodes = _np(out["contact_stencil_nodes"]).reshape(-1, 4)
+    blocks = _np(out["contact_blocks"]).reshape(-1, 90)
+    assert len(nodes) == n
+    worst = 0.0
+    for i, (ids, _g, H, dd, _dp) in enumerate(cs):
+        k = len(ids)
+        assert list(nodes[i, :k]) == list(ids) and np.all(nodes[i, k:] == -1)
+        P, _ = project_eigh(H[None])
+        Hg = lower_blocks_to_full(blocks[i], k)
+        tol = 1e-12 + 4e-15 * np.abs(x).max() / dd  # DESIGN.md contact parity tolerance
+        worst = max(worst, np.linalg.norm(Hg - P[0]) / max(np.linalg.norm(P[0]), 1e-300) / tol)
+    assert worst <= 1.0, worst
+    # SpMV over the full system (static + contact BSR) in the bench's launch configuration
+    N = len(x)
+    A = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
+    assert out["contact_col"].numel() > 0
+    A = A + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
+    v = np.random.default_rng(5).normal(size=3 * N)
+    yg = torch.empty(3 * N, dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)
