@@ -367,10 +367,17 @@ def run_ours(args):
                                 f"extrapolated"}
     ms_newton = ms_max / max(newton, 1)
     npf_ref = None
-    rf = os.path.join(ROOT, "profiles", f"{args.config}_frames.json")
-    if os.path.exists(rf):
-        with open(rf) as f:
-            npf_ref = json.load(f).get("newton_per_frame")
+    long_runs = {}
+    for tag, fn in (("chi=0.3 (scene default)", f"{args.config}_frames.json"), ("chi=0", f"{args.config}_frames_chi0.json")):
+        rf = os.path.join(ROOT, "profiles", fn)
+        if os.path.exists(rf):
+            with open(rf) as f:
+                lr = json.load(f)
+            long_runs[tag] = {k: lr.get(k) for k in ("seconds_per_frame", "newton_per_frame", "frames_converged",
+                                                     "max_newton", "when")}
+            long_runs[tag]["file"] = "profiles/" + fn
+            if tag.startswith("chi=0.3"):
+                npf_ref = lr.get("newton_per_frame")
     line = {
         "metric": METRIC, "value": pcg_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -390,6 +397,7 @@ def run_ours(args):
         "seconds_per_frame": (float(np.mean([f[0] for f in new_frames])) / 1000.0) if new_frames else None,
         "seconds_per_frame_projection": (ms_newton * npf_ref / 1000.0) if npf_ref else None,
         "newton_per_frame_ref": npf_ref,
+        "whole_frame_runs": long_runs or None,
         "max_constraints": tot1["max_constraints"],
         "roofline": {"kernel": "k_spmv (BSR3 SpMV in PCG)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,

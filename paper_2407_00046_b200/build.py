@@ -19,7 +19,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
-         "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC]
+         "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC] + os.environ.get("BAL_NVCC_EXTRA", "").split()
 
 
 def _sources():

@@ -22,9 +22,21 @@
 namespace bal {
 
 constexpr int kSL = 16;        // lanes per block row
-constexpr int kSpmvThreads = 128;
-constexpr int kSpmvMinBlocks = 16;  // 16 x 128 threads resident per SM: independent tile pipelines
-constexpr int kTileRows = 16;  // block rows per SpMV tile
+#ifndef BAL_SPMV_THREADS
+#define BAL_SPMV_THREADS 128
+#endif
+#ifndef BAL_SPMV_MINBLOCKS
+#define BAL_SPMV_MINBLOCKS 16
+#endif
+#ifndef BAL_SPMV_TILE_ROWS
+#define BAL_SPMV_TILE_ROWS 16
+#endif
+#ifndef BAL_SPMV_TILE_CAP
+#define BAL_SPMV_TILE_CAP 320
+#endif
+constexpr int kSpmvThreads = BAL_SPMV_THREADS;
+constexpr int kSpmvMinBlocks = BAL_SPMV_MINBLOCKS;  // 16 x 128 threads resident per SM: independent tile pipelines
+constexpr int kTileRows = BAL_SPMV_TILE_ROWS;  // block rows per SpMV tile
 // persistent grid: exactly the resident CTAs, so the grid-stride sweep visits rows in increasing
 // order wave by wave (the mirror-block L2 reuse above depends on it)
 template <bool DOT, bool MASK>
@@ -53,7 +65,7 @@ static int spmv_grid(int n) {
 // blocks read with evict_last (the earlier row pulls the block, its own row streams it); the grid
 // is persistent (the resident CTAs) and sweeps tiles in increasing order, so both reads of a
 // block fall within one L2 lifetime.
-constexpr int kTileCap = 320;  // blocks staged per chunk
+constexpr int kTileCap = BAL_SPMV_TILE_CAP;  // blocks staged per chunk
 
 BAL_D unsigned long long policy_evict_first() {
   unsigned long long p;
