@@ -385,3 +385,74 @@ def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=20
         xbb = xbb + np.array([fx, top - xbb[:, 1].min() + drop_gap, fz])
         sb.add_body(xbb, tb, 0, v0=(0.0, -1.0, 0.0))
     return sb.build([(E_ball, nu, rho), (E_net, nu, rho)], "C4-puffer-net", chi=chi)
+
+
+# --------------------------------------------------------------------------
+# C2 / C3
+# --------------------------------------------------------------------------
+def _ellipsoid_occ(shape, voxel, shapes):
+    """Union of ellipsoids / capsules on a voxel grid: each entry (kind, a, b, r) with centres in
+    metres; kind 'e' = ellipsoid centre a, semi-axes b; kind 'c' = capsule a->b radius r."""
+    nx, ny, nz = shape
+    g = (np.stack(np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"), -1) + 0.5) * voxel
+    occ = np.zeros(shape, bool)
+    for kind, a, b, r in shapes:
+        a = np.asarray(a, float)
+        b = np.asarray(b, float)
+        if kind == "e":
+            occ |= (((g - a) / b) ** 2).sum(-1) <= 1.0
+        else:
+            ab = b - a
+            t = np.clip(((g - a) @ ab) / (ab @ ab), 0.0, 1.0)
+            occ |= np.linalg.norm(g - (a + t[..., None] * ab), axis=-1) <= r
+    return occ
+
+
+def make_armadillo_like(seed=2, voxel=0.0095, E=1e6, nu=0.4, rho=1e3, chi=0.9, gap=0.01):
+    """C2 recipe: an 'armadillo-like' creature (no paper mesh available: P:672 roller row, 100K tets)
+    = union of 9 ellipsoids / capsules (torso, head, 2 ears, 4 limbs, tail) voxelised, 6 Kuhn tets
+    per voxel, generically rotated, `gap` above a static plane, v0 = (0.5, -1, 0), chi = 0.9."""
+    rng = np.random.default_rng(seed)
+    shapes = [("e", (0.30, 0.28, 0.20), (0.17, 0.11, 0.10), 0),      # torso
+              ("e", (0.50, 0.36, 0.20), (0.07, 0.07, 0.065), 0),     # head
+              ("c", (0.50, 0.41, 0.16), (0.53, 0.50, 0.13), 0.022),  # ears
+              ("c", (0.50, 0.41, 0.24), (0.53, 0.50, 0.27), 0.022),
+              ("c", (0.20, 0.22, 0.12), (0.17, 0.03, 0.09), 0.035),  # legs
+              ("c", (0.20, 0.22, 0.28), (0.17, 0.03, 0.31), 0.035),
+              ("c", (0.40, 0.22, 0.12), (0.44, 0.03, 0.09), 0.035),
+              ("c", (0.40, 0.22, 0.28), (0.44, 0.03, 0.31), 0.035),
+              ("c", (0.14, 0.28, 0.20), (0.02, 0.20, 0.20), 0.03)]   # tail
+    n = (int(0.62 / voxel), int(0.56 / voxel), int(0.42 / voxel))
+    occ = _ellipsoid_occ(n, voxel, shapes)
+    x, t = voxel_mesh(occ, voxel)
+    x = (x - x.mean(0)) @ rot_axis(rng.normal(size=3), np.deg2rad(rng.uniform(2, 5))).T
+    x[:, 1] += -x[:, 1].min() + gap * (1.0 + rng.uniform(0.05, 0.15))
+    sb = SceneBuilder()
+    sb.add_body(x, _orient(x, t), 0, v0=(0.5, -1.0, 0.0))
+    px, pt = _plane(2.0)
+    sb.add_obstacle(px, pt)
+    return sb.build([(E, nu, rho)], "C2-armadillo-like", chi=chi)
+
+
+def make_impact(seed=3, nx=78, ny=8, nz=78, slab_voxel=0.02, R=0.1, sphere_voxel=0.01, E_slab=1e9, E_sphere=1e7,
+                nu=0.4, rho=1e3, gap=0.05, speed=10.0):
+    """C3 recipe: stiff slab nx x ny x nz voxels of slab_voxel (side faces fixed, E = 1 GPa) and a
+    voxelised sphere of radius R (sphere_voxel, E = 1e7) `gap` above it moving at v0 = (0, -speed, 0)
+    (0.33 m/step, so CCD bounds the first steps); both generically rotated by a small angle."""
+    rng = np.random.default_rng(seed)
+    xs, ts = voxel_mesh(np.ones((nx, ny, nz), bool), slab_voxel)
+    c = xs.mean(0)
+    ext = xs.max(0) - xs.min(0)
+    side = (np.abs(xs[:, 0] - c[0]) > 0.5 * ext[0] - 1e-9) | (np.abs(xs[:, 2] - c[2]) > 0.5 * ext[2] - 1e-9)
+    xs = (xs - c) @ rot_axis(rng.normal(size=3), np.deg2rad(rng.uniform(0.2, 0.6))).T
+    m = int(np.ceil(2 * R / sphere_voxel))
+    g = (np.stack(np.meshgrid(np.arange(m), np.arange(m), np.arange(m), indexing="ij"), -1) + 0.5) * sphere_voxel
+    occ = np.linalg.norm(g - R, axis=-1) <= R
+    xb, tb = voxel_mesh(occ, sphere_voxel)
+    xb = (xb - xb.mean(0)) @ random_rotation(rng).T
+    xb[:, 1] += xs[:, 1].max() - xb[:, 1].min() + gap * (1.0 + rng.uniform(0.05, 0.15))
+    xb[:, [0, 2]] += rng.uniform(-0.05, 0.05, 2)
+    sb = SceneBuilder()
+    sb.add_body(xs, _orient(xs, ts), 1, fixed=side.astype(np.uint8))
+    sb.add_body(xb, _orient(xb, tb), 0, v0=(0.0, -speed, 0.0))
+    return sb.build([(E_sphere, nu, rho), (E_slab, nu, rho)], "C3-impact", chi=0.0)
