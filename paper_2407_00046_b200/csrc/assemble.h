@@ -48,6 +48,7 @@ struct StaticPattern {
   int* slot_code = nullptr;  // [16 T] tet*16 + a*4 + b
   // symmetric copy for the SpMV (kernels.h Bsr): lower + diagonal slots in their own CSR
   int nl = 0, nu = 0;
+  int tile_cap_full = 0;  // max full-BSR blocks of an SpMV tile (staged-full mode)
   int* lpos = nullptr;       // [nnzb] position of a full slot in the lower storage, -1 for upper
   int* l_row_ptr = nullptr;  // [n+1]
   int* l_col = nullptr;      // [nl]

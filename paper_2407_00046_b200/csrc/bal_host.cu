@@ -32,6 +32,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.row_ptr = sp.row_ptr;
     b.col = sp.col;
     b.val = sval.ptr;
+    if (spmv_mode() == 2) b.tile_cap_s = sp.tile_cap_full;
   }
   return b;
 }
@@ -345,7 +346,11 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     c->sp.u_col = c->sp_ucol.ptr;
     c->sp_sym = spmv_symmetric_enabled();
     if (c->sp_sym) c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1));
+    for (int r0 = 0; r0 < N; r0 += kSpmvTileRows)
+      c->sp.tile_cap_full = std::max(c->sp.tile_cap_full,
+                                     row_ptr[std::min(N, r0 + kSpmvTileRows)] - row_ptr[r0]);
     spmv_init_grids();
+    spmv_prepare(c->static_bsr());
   }
   c->sval.reserve(9 * (size_t)nnzb);
   c->stage_e.reserve(90 * (size_t)std::max(T, 1));

@@ -28,15 +28,12 @@ constexpr int kSL = 16;        // lanes per block row
 #ifndef BAL_SPMV_MINBLOCKS
 #define BAL_SPMV_MINBLOCKS 16
 #endif
-#ifndef BAL_SPMV_TILE_ROWS
-#define BAL_SPMV_TILE_ROWS 16
-#endif
 #ifndef BAL_SPMV_TILE_CAP
 #define BAL_SPMV_TILE_CAP 320
 #endif
 constexpr int kSpmvThreads = BAL_SPMV_THREADS;
 constexpr int kSpmvMinBlocks = BAL_SPMV_MINBLOCKS;  // 16 x 128 threads resident per SM: independent tile pipelines
-constexpr int kTileRows = BAL_SPMV_TILE_ROWS;  // block rows per SpMV tile
+constexpr int kTileRows = kSpmvTileRows;  // block rows per SpMV tile
 // persistent grid: exactly the resident CTAs, so the grid-stride sweep visits rows in increasing
 // order wave by wave (the mirror-block L2 reuse above depends on it)
 template <bool DOT, bool MASK>
@@ -222,6 +219,168 @@ k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_spmv_sf ("staged full"): full static BSR (both triangles stored), each 16-row tile's blocks and
+// columns are one contiguous range, copied to shared memory with 16-byte cp.async (L2 evict_first)
+// one tile ahead while the CTA computes the previous tile from shared memory; only v (L2-resident)
+// and the few contact blocks are gathered.  More bytes than the symmetric layout, but a pure
+// streaming access pattern (no mirror gathers, no strided LSU traffic on the values).
+BAL_D void cp_async16(void* dst, const void* src, unsigned long long pol) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "l"(pol));
+}
+BAL_D void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+BAL_D void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+struct SfLayout {
+  size_t o_sc, stride, o_contrib, o_rp, total;
+  BAL_HD void init(int cap) {
+    auto up16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    o_sc = up16((size_t)(cap * 9 + 4) * 8);
+    stride = up16(o_sc + (size_t)(cap + 8) * 4);
+    o_contrib = 2 * stride;
+    o_rp = up16(o_contrib + (size_t)cap * 24);
+    total = up16(o_rp + 2 * (kTileRows + 1) * 4);
+  }
+};
+
+BAL_D int stage_range(unsigned char* dst, const void* src, long long lo, long long hi, int esz,
+                      unsigned long long pol) {
+  if (hi <= lo) return 0;
+  const size_t b0 = (size_t)lo * esz, b1 = (size_t)hi * esz;
+  const size_t a0 = b0 & ~(size_t)15;
+  const int nch = (int)((b1 - a0 + 15) >> 4);
+  for (int c = threadIdx.x; c < nch; c += blockDim.x)
+    cp_async16(dst + 16 * (size_t)c, (const unsigned char*)src + a0 + 16 * (size_t)c, pol);
+  return (int)((b0 - a0) / esz);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(kSpmvThreads)
+k_spmv_sf(Bsr S, Bsr C, const double* __restrict__ v, double* __restrict__ y, double* partials, unsigned* counter,
+          PcgScal* sc) {
+  if (DOT && sc->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SfLayout Lo;
+  Lo.init(S.tile_cap_s);
+  int(*rp)[kTileRows + 1] = reinterpret_cast<int(*)[kTileRows + 1]>(smraw + Lo.o_rp);
+  double(*contrib)[3] = reinterpret_cast<double(*)[3]>(smraw + Lo.o_contrib);
+  const int n = S.n;
+  const int tid = threadIdx.x;
+  const unsigned long long pol_first = policy_evict_first();
+  const int ntiles = (n + kTileRows - 1) / kTileRows;
+  const int* crp = C.nnzb > 0 ? C.row_ptr : nullptr;
+  int offv[2] = {0, 0}, offc[2] = {0, 0};
+  auto load_rp = [&](int tile, int buf) {
+    const int r0 = tile * kTileRows, R = min(kTileRows, n - r0);
+    for (int k = tid; k <= kTileRows; k += blockDim.x) rp[buf][k] = __ldg(S.row_ptr + r0 + min(k, R));
+  };
+  auto issue = [&](int buf) {
+    unsigned char* base = smraw + buf * Lo.stride;
+    const int s0 = rp[buf][0], s1 = rp[buf][kTileRows];
+    offv[buf] = stage_range(base, S.val, 9ll * s0, 9ll * s1, 8, pol_first);
+    offc[buf] = stage_range(base + Lo.o_sc, S.col, s0, s1, 4, pol_first);
+  };
+  double dacc = 0.0;
+  int tile = blockIdx.x;
+  if (tile < ntiles) {
+    load_rp(tile, 0);
+    __syncthreads();
+    issue(0);
+  }
+  cp_async_commit();
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int buf = it & 1;
+    const int t1 = tile + gridDim.x;
+    if (t1 < ntiles) {
+      load_rp(t1, buf ^ 1);
+      __syncthreads();
+      issue(buf ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const int r0 = tile * kTileRows, R = min(kTileRows, n - r0);
+    const unsigned char* base = smraw + buf * Lo.stride;
+    const double* sv = reinterpret_cast<const double*>(base) + offv[buf];
+    const int* scl = reinterpret_cast<const int*>(base + Lo.o_sc) + offc[buf];
+    const int s0 = rp[buf][0], nS = rp[buf][kTileRows] - s0;
+    const int ni = 3 * nS;
+#pragma unroll 4
+    for (int k = tid; k < ni; k += blockDim.x) {
+      const int b = k / 3, r = k - 3 * (k / 3);
+      const double* a = sv + 9 * b + 3 * r;
+      const double* __restrict__ vc = v + 3 * (size_t)scl[b];
+      contrib[b][r] = fma(a[2], __ldg(vc + 2), fma(a[1], __ldg(vc + 1), a[0] * __ldg(vc)));
+    }
+    __syncthreads();
+    if (tid < 3 * R) {
+      const int row = tid / 3, r = tid - 3 * (tid / 3);
+      double acc = 0.0;
+      for (int b = rp[buf][row] - s0; b < rp[buf][row + 1] - s0; ++b) acc += contrib[b][r];
+      if (crp) {
+        for (int s2 = __ldg(crp + r0 + row); s2 < __ldg(crp + r0 + row + 1); ++s2) {
+          const double* a = C.val + 9 * (size_t)s2 + 3 * r;
+          const double* vc = v + 3 * (size_t)__ldg(C.col + s2);
+          acc += fma(a[2], vc[2], fma(a[1], vc[1], a[0] * vc[0]));
+        }
+      }
+      y[3 * (size_t)(r0 + row) + r] = acc;
+      if (DOT) dacc += v[3 * (size_t)(r0 + row) + r] * acc;
+    }
+    __syncthreads();
+  }
+  if (DOT) {
+    __shared__ double sh[kSpmvThreads / 32];
+    __shared__ bool last;
+    const double bs = block_sum<kSpmvThreads>(dacc, sh);
+    if (threadIdx.x == 0) {
+      partials[blockIdx.x] = bs;
+      __threadfence();
+      last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      double t = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += partials[i];
+      t = block_sum<kSpmvThreads>(t, sh);
+      if (threadIdx.x == 0) {
+        sc->pq = t;
+        sc->alpha = sc->rz / t;
+        *counter = 0u;
+      }
+    }
+  }
+}
+
+template <bool DOT>
+static int spmv_sf_grid(const Bsr& S, size_t& smem) {
+  SfLayout Lo;
+  Lo.init(S.tile_cap_s);
+  smem = Lo.total;
+  static int per_sm[2] = {-1, -1};
+  static size_t smem_at[2] = {0, 0};
+  const int key = DOT ? 1 : 0;
+  if (per_sm[key] < 0 || smem_at[key] != smem) {
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_spmv_sf<DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[key], k_spmv_sf<DOT>, kSpmvThreads, smem));
+    smem_at[key] = smem;
+  }
+  if (per_sm[key] <= 0) return 0;
+  return std::max(1, std::min(per_sm[key] * kSMs, ceil_div((long long)S.n, kTileRows)));
+}
+
+static bool spmv_sf_usable(const Bsr& S) { return !S.m_row_ptr && S.tile_cap_s > 0 && S.tile_cap_s <= 2048; }
+
+void spmv_prepare(const Bsr& S) {  // occupancy / smem attribute outside any stream capture
+  if (!spmv_sf_usable(S)) return;
+  size_t sm = 0;
+  (void)spmv_sf_grid<false>(S, sm);
+  (void)spmv_sf_grid<true>(S, sm);
+}
+
 void spmv_init_grids() {  // occupancy queries outside any stream capture (called by bal_init)
   (void)spmv_grid<false, false>(1);
   (void)spmv_grid<true, false>(1);
@@ -230,6 +389,15 @@ void spmv_init_grids() {  // occupancy queries outside any stream capture (calle
 
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y) {
   if (S.n <= 0) return;
+  if (spmv_sf_usable(S)) {
+    size_t sm = 0;
+    const int g = spmv_sf_grid<false>(S, sm);
+    if (g > 0) {
+      k_spmv_sf<false><<<g, kSpmvThreads, sm, st>>>(S, C, v, y, nullptr, nullptr, nullptr);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   const int blocks = spmv_grid<false, false>(S.n);
   k_spmv<false, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, nullptr, nullptr, nullptr, nullptr);
   CK(cudaGetLastError());
@@ -237,6 +405,15 @@ void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, d
 
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* partials,
                      unsigned* counter, PcgScal* sc) {
+  if (spmv_sf_usable(S)) {
+    size_t sm = 0;
+    const int g = spmv_sf_grid<true>(S, sm);
+    if (g > 0) {
+      k_spmv_sf<true><<<g, kSpmvThreads, sm, st>>>(S, C, v, y, partials, counter, sc);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   const int blocks = spmv_grid<true, false>(S.n);
   k_spmv<true, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, partials, counter, sc, nullptr);
   CK(cudaGetLastError());

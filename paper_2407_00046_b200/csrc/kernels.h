@@ -6,6 +6,11 @@
 
 namespace bal {
 
+#ifndef BAL_SPMV_TILE_ROWS
+#define BAL_SPMV_TILE_ROWS 16
+#endif
+constexpr int kSpmvTileRows = BAL_SPMV_TILE_ROWS;  // block rows per SpMV tile
+
 constexpr int kElasticThreads = 128;
 constexpr int kMaxGroups = 64;
 
@@ -41,11 +46,21 @@ struct Bsr {
   const int* m_pos = nullptr;      // [m_row_ptr[n]]
   const int* m_col = nullptr;      // [m_row_ptr[n]]
   int nmirror = 0;
+  int tile_cap_s = 0;  // staged-full mode: max blocks of a kTileRows-row tile (0 = not staged)
 };
-inline bool spmv_symmetric_enabled() {
-  static const bool full = getenv("BAL_SPMV_FULL") != nullptr;  // A/B switch: full static BSR in the SpMV
-  return !full;
+// static-part SpMV layout: 0 = symmetric (lower + mirror index), 1 = full BSR streamed by the tiled
+// kernel, 2 = full BSR staged through shared memory with cp.async.  BAL_SPMV=sym|full|staged.
+inline int spmv_mode() {
+  static const int m = [] {
+    const char* e = getenv("BAL_SPMV");
+    if (e && e[0] == 'f') return 1;
+    if (e && e[0] == 's' && e[1] == 't') return 2;
+    if (e && e[0] == 's') return 0;
+    return getenv("BAL_SPMV_FULL") ? 1 : 0;
+  }();
+  return m;
 }
+inline bool spmv_symmetric_enabled() { return spmv_mode() == 0; }
 
 // PCG scalars living in device memory (single group)
 struct PcgScal {
@@ -63,6 +78,7 @@ struct GrpScal {
 };
 
 void spmv_init_grids();
+void spmv_prepare(const Bsr& S);
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y);
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,
                      double* partials, unsigned* counter, PcgScal* sc);
