@@ -322,6 +322,23 @@ def run_ours(args):
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+    # SURVEY d.1 (b): PCG microbenchmark on the live (last assembled) C4 system: 1,000 global PCG
+    # iterations, termination disabled, CUDA events (outside the timed region)
+    pcg_micro = None
+    try:
+        b = torch.randn(x.numel(), dtype=torch.float64, device=dev)
+        xo = torch.empty_like(b)
+        z0 = torch.zeros_like(b)
+        bal.bal_pcg(ctx, b, z0, xo, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=50)  # warm-up
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        sm = bal.bal_pcg(ctx, b, z0, xo, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=1000)
+        m1.record(stream)
+        torch.cuda.synchronize()
+        pcg_micro = {"iters": int(sm["iters"]), "ms": m0.elapsed_time(m1),
+                     "iters_per_s": 1000.0 * sm["iters"] / m0.elapsed_time(m1)}
+    except Exception as ex:  # noqa: BLE001 -- reported, never fatal for the main line
+        pcg_micro = {"error": str(ex)}
     # e2e through the public API with host buffers: pinned x_t, v_t -> device, the same number of
     # Newton iterations of a frame, x back to the host, all inside the timed region
     e2e = None
@@ -388,6 +405,7 @@ def run_ours(args):
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (system ~0.5 GB/PCG iteration)"},
         "pcg_iters_per_s_in_pcg": pcg / (d["ms_pcg"] / 1000.0) if d["ms_pcg"] > 0 else None,
+        "pcg_microbench": pcg_micro,
         "newton_iters": newton, "pcg_iters": pcg, "pcg_iters_per_newton": ppn,
         "ms_per_newton": ms_newton,
         "phase_ms_per_newton": {k: d[k] / max(newton, 1) for k in
