@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c4", "c1"])
+    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -53,6 +53,8 @@ def make_scene(cfg):
     import scenes
     if cfg == "c1":
         return scenes.make_cubes(1), "C1 two stacked soft cubes (1.5K tets), dt=1/30 s"
+    if cfg == "c5":
+        return scenes.make_puffer_tiles(5), "C5 3x2 replicated puffer-net tiles (~10.5M tets) on ONE GPU, dt=1/30 s"
     return scenes.make_puffer_net(seed=4), "C4 puffer balls on chain-net (~1.7M tets), dt=1/30 s"
 
 

@@ -456,3 +456,31 @@ def make_impact(seed=3, nx=78, ny=8, nz=78, slab_voxel=0.02, R=0.1, sphere_voxel
     sb.add_body(xs, _orient(xs, ts), 1, fixed=side.astype(np.uint8))
     sb.add_body(xb, _orient(xb, tb), 0, v0=(0.0, -speed, 0.0))
     return sb.build([(E_sphere, nu, rho), (E_slab, nu, rho)], "C3-impact", chi=0.0)
+
+
+def make_puffer_tiles(seed=5, tiles=(3, 2), gap=0.1, **kw):
+    """C5 recipe (configs[4]): the C4 tile replicated tiles[0] x tiles[1] in the x-z plane with `gap`
+    metres between tiles, tile i generated with seed 500 + i (its own fixed border frame, balls,
+    jitter); ~10.5M tets for 3 x 2."""
+    del seed  # the per-tile seeds are 500 + i (SURVEY d.2)
+    parts = []
+    off = np.zeros(3)
+    k = 0
+    for i in range(tiles[0]):
+        for j in range(tiles[1]):
+            sc = make_puffer_net(seed=500 + k, **kw)
+            parts.append((sc, np.array([i, 0.0, j])))
+            k += 1
+    span = parts[0][0]["rest_x"].max(0) - parts[0][0]["rest_x"].min(0) + gap
+    sb = SceneBuilder()
+    for sc, ij in parts:
+        off = ij * span
+        x = sc["rest_x"] + off
+        sb.x.append(x)
+        sb.tets.append(sc["tets"].astype(np.int64) + sb.n)
+        sb.mat.append(sc["tet_material"])
+        sb.fixed.append(sc["node_fixed"])
+        sb.v.append(sc["v0"])
+        sb.n += len(x)
+    first = parts[0][0]
+    return sb.build(first["materials"], "C5-puffer-tiles", chi=first["params"]["chi"])
