@@ -591,7 +591,7 @@ __global__ void k_pcg_pupdate(int n3, const double* __restrict__ z, double* __re
 // barrier (cooperative launch: the grid is co-resident), every CTA re-reduces the partials in the
 // same fixed order (identical beta everywhere, deterministic), CTA 0 updates the scalars and the
 // App. B stop test, then p = z + beta p.  Saves the z round trip and one launch per iteration.
-constexpr int kFuseMax = 8;  // nodes per thread held in registers
+template <int kFuseMax>  // nodes per thread held in registers
 __global__ void __launch_bounds__(kVecThreads)
 k_pcg_update_fused(int n, const double* __restrict__ dinv, double* __restrict__ p, const double* __restrict__ q,
                    double* __restrict__ x, double* __restrict__ r, double* partials, PcgScal* sc, double* hist) {
@@ -658,23 +658,39 @@ k_pcg_update_fused(int n, const double* __restrict__ dinv, double* __restrict__ 
   }
 }
 
-// grid for the fused update, 0 when it cannot hold n nodes (caller falls back to update + pupdate)
-int pcg_fused_grid(int n) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    const bool off = getenv("BAL_PCG_UNFUSED") != nullptr;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_update_fused, kVecThreads, 0));
-    if (off) per_sm = 0;
+// grid and variant (nodes per thread) for the fused update: the smallest register footprint whose
+// co-resident grid holds n nodes; 0 when none does (caller falls back to update + p-update)
+static int fused_per_sm(int K) {
+  static int per[2] = {-1, -1};
+  const int i = K == 4 ? 0 : 1;
+  if (per[i] < 0) {
+    if (K == 4) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[i], k_pcg_update_fused<4>, kVecThreads, 0));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[i], k_pcg_update_fused<8>, kVecThreads, 0));
   }
-  const long long cap = (long long)per_sm * kSMs * kVecThreads * kFuseMax;
-  if (per_sm <= 0 || n > cap) return 0;
-  return std::min(per_sm * kSMs, std::max(1, ceil_div((long long)n, (long long)kVecThreads * kFuseMax)));
+  return per[i];
+}
+
+int pcg_fused_grid(int n, int* kvariant) {
+  static const bool off = getenv("BAL_PCG_UNFUSED") != nullptr;
+  if (off) return 0;
+  for (int K : {4, 8}) {
+    const int per_sm = fused_per_sm(K);
+    const long long cap = (long long)per_sm * kSMs * kVecThreads * K;
+    if (per_sm > 0 && n <= cap) {
+      if (kvariant) *kvariant = K;
+      return std::min(per_sm * kSMs, std::max(1, ceil_div((long long)n, (long long)kVecThreads * K)));
+    }
+  }
+  return 0;
 }
 
 void launch_pcg_update_fused(cudaStream_t st, int grid, int n, const double* dinv, double* p, const double* q,
                              double* x, double* r, double* partials, PcgScal* sc, double* hist) {
+  int K = 8;
+  (void)pcg_fused_grid(n, &K);
   void* args[] = {&n, &dinv, &p, &q, &x, &r, &partials, &sc, &hist};
-  CK(cudaLaunchCooperativeKernel((const void*)k_pcg_update_fused, dim3(grid), dim3(kVecThreads), args, 0, st));
+  const void* fn = K == 4 ? (const void*)k_pcg_update_fused<4> : (const void*)k_pcg_update_fused<8>;
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kVecThreads), args, 0, st));
 }
 
 void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc) {

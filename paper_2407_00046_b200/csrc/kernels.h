@@ -89,7 +89,7 @@ void launch_pcg_update(cudaStream_t st, int n, const double* dinv, const double*
                        double* x, double* r, double* z, double* partials, unsigned* counter, PcgScal* sc,
                        double* hist);
 void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc);
-int pcg_fused_grid(int n);
+int pcg_fused_grid(int n, int* kvariant = nullptr);
 void launch_pcg_update_fused(cudaStream_t st, int grid, int n, const double* dinv, double* p, const double* q,
                              double* x, double* r, double* partials, PcgScal* sc, double* hist);
 
