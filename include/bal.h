@@ -238,10 +238,11 @@ bal_status bal_bench_spmv(bal_ctx* ctx, int32_t iters, double* mean_us);
 #define BAL_TRACE_FIELDS 15
 int32_t bal_get_trace(const bal_ctx* ctx, double* out, int32_t max_records);
 
-/* SpMV instrumentation accumulated over every PCG SpMV launch since ctx creation (CUDA events
- * bracketing each launch on the ctx stream): out[0] = total kernel milliseconds, out[1] = number
- * of launches, out[2] = algorithmic bytes (72N + 76E + 4(N+1) + 80C + 48N summed
- * over launches), out[3] = bytes the full-BSR layout must move at minimum.  HOST out[4]. */
+/* SpMV instrumentation accumulated over the timed PCG SpMV launches since ctx creation (CUDA event
+ * record nodes bracketing the first SpMV of every 8-iteration PCG graph batch on the ctx stream, a
+ * live 1-in-8 sample): out[0] = total kernel milliseconds, out[1] = number of timed launches,
+ * out[2] = algorithmic bytes (72N + 76E + 4(N+1) + 80C + 48N summed over them),
+ * out[3] = bytes the configured SpMV layout must move at minimum (summed likewise).  HOST out[4]. */
 bal_status bal_spmv_counters(const bal_ctx* ctx, double* out);
 
 /* Counters of kernels launched by the library since ctx creation (bench's gpu_launches). */
