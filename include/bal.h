@@ -61,6 +61,8 @@ typedef struct { double E, nu, rho; } bal_material;
 /* Flags */
 #define BAL_NO_WARMSTART 1u  /* ablation: global PCG from x0 = 0 */
 #define BAL_NO_AUGLAG 2u     /* ablation: A' = {} and sigma = sigma0 (plain IPC barrier Newton) */
+#define BAL_FRICTION_LAGGED 4u /* ablation (GPU only, no oracle parity): friction anchors (lambda, n, beta)
+                                * of the frame's first iterate kept for the whole frame */
 
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {

@@ -13,11 +13,11 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (BAL_NO_AUGLAG, BAL_NO_WARMSTART, STATUS, bal_bsr_host, bal_contact_state, bal_material,
+from ._lib import (BAL_FRICTION_LAGGED, BAL_NO_AUGLAG, BAL_NO_WARMSTART, STATUS, bal_bsr_host, bal_contact_state, bal_material,
                    bal_mesh, bal_params, bal_pcg_opts, bal_pcg_stats, bal_step_stats, bal_system_view)
 
 __all__ = ["BalError", "BalCtx", "bal_init", "bal_step", "bal_step_host", "bal_assemble", "bal_spmv", "bal_pcg",
-           "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG", "lib_path"]
+           "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG", "BAL_FRICTION_LAGGED", "lib_path"]
 
 lib_path = _lib.LIB_PATH
 

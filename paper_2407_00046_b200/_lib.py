@@ -25,6 +25,7 @@ STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_MESH", -3: "INFEASIBLE", -4: "NOT
           -5: "CONSTRAINT_BUDGET", -6: "CUDA", -7: "NCCL", -8: "OOM", -9: "NAN"}
 BAL_NO_WARMSTART = 1
 BAL_NO_AUGLAG = 2
+BAL_FRICTION_LAGGED = 4
 
 
 class bal_mesh(C.Structure):

@@ -496,9 +496,11 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
     // contact stencils = A u A' (Q22)
     t0 = clk::now();
     stencil_union(st, c->ks, w.cs_A.n, w.cs_A.keys.ptr, w.n_ap, w.ap_keys.ptr, w.ap_mu.ptr, w.ap_s.ptr, c->cset);
-    // friction anchors at x^l
-    c->n_fric = 0;
-    if (P.chi > 0.0 && c->cset.n > 0) {
+    // friction anchors at x^l; ablation BAL_FRICTION_LAGGED: anchors of the frame's first
+    // iterate kept for the whole frame (IPC's lagged, semi-implicit friction)
+    const bool lagged = (P.flags & BAL_FRICTION_LAGGED) != 0;
+    if (!lagged || l == 0) c->n_fric = 0;
+    if (P.chi > 0.0 && c->cset.n > 0 && (!lagged || l == 0)) {
       const int nc = c->cset.n;
       c->fr_keys.reserve(5 * (size_t)nc);
       c->fr_gam.reserve(4 * (size_t)nc);

@@ -27,7 +27,8 @@ def main():
     if "--max-newton" in sys.argv:
         sc["params"]["max_newton"] = int(sys.argv[sys.argv.index("--max-newton") + 1])
     dev = torch.device("cuda:0")
-    ctx = bal.bal_init(sc)
+    flags = bal.BAL_FRICTION_LAGGED if "--lagged-friction" in sys.argv else 0
+    ctx = bal.bal_init(sc, flags=flags)
     st = torch.cuda.current_stream(dev)
     x = torch.as_tensor(sc["x0"].ravel(), device=dev)
     v = torch.as_tensor(sc["v0"].ravel(), device=dev)
@@ -53,7 +54,7 @@ def main():
         x, v = xn, vn
     conv = [fr for fr in frames if fr["converged"]]
     res = {"scene": "C4 puffer-net (scenes.make_puffer_net(seed=4" + "".join(f", {k}={v}" for k, v in kw.items())
-                    + "))", "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+                    + "))" + (" with BAL_FRICTION_LAGGED" if flags else ""), "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
            "gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
            "frames": frames,
            "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in frames])),
