@@ -247,6 +247,21 @@ int32_t bal_get_trace(const bal_ctx* ctx, double* out, int32_t max_records);
  * out[3] = bytes the configured SpMV layout must move at minimum (summed likewise).  HOST out[4]. */
 bal_status bal_spmv_counters(const bal_ctx* ctx, double* out);
 
+/* ----------------------------------------------------------------------------------------
+ * Vertex-domain partition, host logic of the multi-GPU path.  HOST arrays, no
+ * CUDA calls, callable without a GPU.
+ * bal_partition_rows: contiguous block-row ranges [bounds[k], bounds[k+1]), k < world, balanced
+ *   by row_cost[i] >= 0 (e.g. stored + mirror blocks the SpMV touches in row i); bounds[world+1].
+ *   Errors: BAL_E_INVALID_ARG.
+ * bal_ghost_columns: the sorted unique columns referenced by rows [r0, r1) of the CSR pattern
+ *   (row_ptr[n+1], col) that lie outside [r0, r1) -- the values a rank owning [r0, r1) receives
+ *   before each SpMV.  Writes min(count, cap) entries to out (may be NULL) and returns the count,
+ *   or BAL_E_INVALID_ARG (< 0).
+ * --------------------------------------------------------------------------------------*/
+bal_status bal_partition_rows(int32_t n, const int64_t* row_cost, int32_t world, int32_t* bounds);
+int32_t bal_ghost_columns(int32_t n, const int32_t* row_ptr, const int32_t* col, int32_t r0, int32_t r1,
+                          int32_t* out, int32_t cap);
+
 /* Counters of kernels launched by the library since ctx creation (bench's gpu_launches). */
 int64_t bal_kernel_launches(const bal_ctx* ctx);
 

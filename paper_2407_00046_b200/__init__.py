@@ -325,3 +325,25 @@ def bal_bench_spmv(ctx, iters):
     us = C.c_double()
     _check(ctx, _lib.lib.bal_bench_spmv(ctx.handle, iters, C.byref(us)))
     return us.value
+
+
+def bal_partition_rows(row_cost, world):
+    """Contiguous block-row ranges balanced by row_cost; returns bounds (world+1,)."""
+    rc = np.ascontiguousarray(row_cost, np.int64)
+    b = np.zeros(world + 1, np.int32)
+    _check(None, _lib.lib.bal_partition_rows(len(rc), _lib.ptr(rc, C.c_int64), int(world), _lib.ptr(b, C.c_int32)))
+    return b
+
+
+def bal_ghost_columns(row_ptr, col, r0, r1):
+    """Sorted unique columns of rows [r0, r1) outside [r0, r1) (the per-SpMV ghost values)."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    cl = np.ascontiguousarray(col, np.int32)
+    n = len(rp) - 1
+    m = _lib.lib.bal_ghost_columns(n, _lib.ptr(rp, C.c_int32), _lib.ptr(cl, C.c_int32), int(r0), int(r1), None, 0)
+    if m < 0:
+        raise BalError(m, "bal_ghost_columns")
+    out = np.zeros(max(m, 1), np.int32)
+    _lib.lib.bal_ghost_columns(n, _lib.ptr(rp, C.c_int32), _lib.ptr(cl, C.c_int32), int(r0), int(r1),
+                               _lib.ptr(out, C.c_int32), m)
+    return out[:m]
