@@ -23,7 +23,10 @@ def main():
     if "--chi" in sys.argv:
         kw["chi"] = float(sys.argv[sys.argv.index("--chi") + 1])
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join("profiles", "c4_frames.json")
-    sc = scenes.make_puffer_net(seed=4, **kw)
+    scene = sys.argv[sys.argv.index("--scene") + 1] if "--scene" in sys.argv else "c4"
+    make = {"c4": lambda: scenes.make_puffer_net(seed=4, **kw), "c2": lambda: scenes.make_armadillo_like(2, **kw),
+            "c3": lambda: scenes.make_impact(3, **kw), "c1": lambda: scenes.make_cubes(1)}[scene]
+    sc = make()
     if "--max-newton" in sys.argv:
         sc["params"]["max_newton"] = int(sys.argv[sys.argv.index("--max-newton") + 1])
     dev = torch.device("cuda:0")
@@ -53,8 +56,8 @@ def main():
         print(json.dumps(rec), flush=True)
         x, v = xn, vn
     conv = [fr for fr in frames if fr["converged"]]
-    res = {"scene": "C4 puffer-net (scenes.make_puffer_net(seed=4" + "".join(f", {k}={v}" for k, v in kw.items())
-                    + "))" + (" with BAL_FRICTION_LAGGED" if flags else ""), "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+    res = {"scene": sc["name"] + "".join(f", {k}={v}" for k, v in kw.items())
+                    + (" with BAL_FRICTION_LAGGED" if flags else ""), "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
            "gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
            "frames": frames,
            "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in frames])),
