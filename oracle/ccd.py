@@ -20,7 +20,8 @@ DESIGN.md reading R-CCD1:
     R-CCD1: the root itself is the coplanar configuration whose signed distance is rounding
     noise, so the TOI is backtracked at least once: toi = 0.9 t, then while the signed distance
     at toi and at t_ref differ in sign (PT/EE-resolved pairs only; PP/PE lack a signed distance),
-    toi <- 0.9 toi (<= 200 times, then 0).
+    toi <- 0.9 toi (<= 200 times, then 0); R-CCD3: if toi falls to or below the previous
+    (non-contact) root t_prev, the sign can never match again, so toi = t_ref.
  5. identically-zero cubic: toi = 0.9 d(0) / (max_k |dx_k| of feature A + of feature B) (Q33).
 Returns toi in [0,1] (1.0 = no collision on this step).
 """
@@ -155,6 +156,9 @@ def pair_toi(ftype, x, dx, ids, dhat):
                 while (_signed_dist(ftype, X0 + toi * DX) > 0) != (sref > 0):
                     toi *= 0.9
                     n += 1
+                    if toi <= t_prev:  # DESIGN.md R-CCD3: crossed back over an earlier, non-contact root
+                        toi = tref
+                        break
                     if n >= 200:
                         toi = 0.0
                         break

@@ -310,6 +310,10 @@ BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat) {
           for (int k = 0; k < 4; ++k) Q[k] = X0[k] + toi * DX[k];
           if ((signed_dist(ftype, Q) > 0) == sref) break;
           toi *= 0.9;
+          if (toi <= t_prev) {  // DESIGN.md R-CCD3: crossed back over an earlier, non-contact root
+            toi = tref;
+            break;
+          }
           if (++n >= 200) {
             toi = 0.0;
             break;
