@@ -63,6 +63,13 @@ typedef struct { double E, nu, rho; } bal_material;
 #define BAL_NO_AUGLAG 2u     /* ablation: A' = {} and sigma = sigma0 (plain IPC barrier Newton) */
 #define BAL_FRICTION_LAGGED 4u /* ablation (GPU only, no oracle parity): friction anchors (lambda, n, beta)
                                 * of the frame's first iterate kept for the whole frame */
+#define BAL_SIGMA_CAP 8u     /* NEXT-1 ablation: sigma schedule of Alg. 1 line 16 with an overall ceiling
+                              * of 1e8 sigma^0 (the capped reading of Q8) */
+#define BAL_SIGMA_MIN 16u    /* reading of Alg. 1 line 16 with min instead of the printed max:
+                              * sigma <- min(1.2 sigma, 100 sigma^0), IPC-style capped growth */
+#define BAL_FRICTION_NO_FREEZE 32u /* literal per-iteration friction anchors for the whole step: disables the
+                                    * R-FRIC1 freeze (anchors frozen once min ||e|| has not halved in 10
+                                    * Newton iterations) */
 
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {
@@ -81,7 +88,7 @@ typedef struct {
   int32_t max_newton;    /* 1000 (Q13) */
   int32_t max_pcg;       /* 20000 (Q16) */
   int64_t max_constraints; /* constraint budget, P:440 (Q36) */
-  uint32_t flags;        /* BAL_NO_WARMSTART | BAL_NO_AUGLAG */
+  uint32_t flags;        /* BAL_NO_WARMSTART | BAL_NO_AUGLAG | BAL_FRICTION_LAGGED | BAL_SIGMA_CAP */
 } bal_params;
 
 /* Per-step statistics (Table 1 columns "avg. #iters (Newton)", "#cons"). */
@@ -95,12 +102,49 @@ typedef struct {
   double ms_total, ms_collision, ms_assembly, ms_warmstart, ms_pcg, ms_linesearch;
 } bal_step_stats;
 
+/* Multi-GPU: one process per GPU, every call collective across the ranks.  The mesh
+ * is partitioned into contiguous vertex (block-row) ranges balanced by SpMV cost and aligned to the
+ * SpMV tile (bal_dist_info); each rank assembles the whole system (replicated stencils, identical
+ * bits on every rank) and the global PCG / warm start are distributed: a rank computes only its
+ * owned rows, receives the ghost entries of p before every SpMV (boundary-only halo of the block
+ * rows its rows touch, static pattern + this Newton iteration's contact pattern) and all-reduces
+ * the PCG dot products (P:381 domain-masked SpMV, P:416-423 storage; App. B decisions are taken
+ * from the all-reduced scalars, so all ranks run the same iterations).  The solution slices are
+ * all-gathered once per Newton iteration for the replicated line search.
+ * Transport: NCCL (nccl_unique_id = the 128-byte id from bal_nccl_unique_id on rank 0, broadcast
+ * by the caller, e.g. over torch.distributed) or, when host_allreduce / host_exchange are set, a
+ * host transport (the library synchronises its stream and calls them on HOST buffers; tests).
+ *  host_allreduce(buf, n, user): in-place elementwise sum of n doubles over the ranks; 0 = OK.
+ *  host_exchange(send, send_counts, recv, recv_counts, user): counts[world] in doubles; send/recv
+ *    are packed in peer order; every rank sends send[peer block] to peer and receives recv[peer
+ *    block] from it; 0 = OK. */
+typedef int32_t (*bal_host_allreduce_fn)(double* buf, int32_t n, void* user);
+typedef int32_t (*bal_host_exchange_fn)(const double* send, const int32_t* send_counts, double* recv,
+                                        const int32_t* recv_counts, void* user);
+typedef struct {
+  int32_t rank, world, device;
+  const void* nccl_unique_id;        /* 128 bytes, or NULL with the host transport */
+  bal_host_allreduce_fn host_allreduce;
+  bal_host_exchange_fn host_exchange;
+  void* user;
+} bal_dist;
+
+/* Writes a fresh NCCL unique id (128 bytes) to out (rank 0 calls it and broadcasts the bytes).
+ * Errors: BAL_E_INVALID_ARG, BAL_E_NCCL. */
+bal_status bal_nccl_unique_id(void* out128);
+
 /* Create a context: validates the mesh, precomputes D_m^{-1}, volumes, lumped masses,
  * surface triangles / edges, the static BSR pattern and the atomic-free slot lists, and uploads
- * everything to `device`.  Errors: BAL_E_INVALID_ARG, BAL_E_BAD_MESH, BAL_E_CUDA, BAL_E_OOM.
- * On error *out is NULL. */
+ * everything to dist->device (dist NULL = one GPU, device 0; world 1 = one GPU, no collectives).
+ * With world > 1 also creates the communicator and the partition (collective over the ranks).
+ * Errors: BAL_E_INVALID_ARG, BAL_E_BAD_MESH, BAL_E_CUDA, BAL_E_NCCL, BAL_E_OOM.  On error *out is
+ * NULL. */
 bal_status bal_init(const bal_mesh* mesh, const bal_material* materials, int32_t n_materials,
-                    const bal_params* params, int32_t device, bal_ctx** out);
+                    const bal_params* params, const bal_dist* dist, bal_ctx** out);
+
+/* Owned block rows [*r0, *r1) of this rank and the halo of its last global PCG solve (nodes sent /
+ * received per SpMV, summed over peers).  Any pointer may be NULL. */
+bal_status bal_dist_info(const bal_ctx* ctx, int32_t* r0, int32_t* r1, int64_t* halo_send, int64_t* halo_recv);
 
 /* Use `cuda_stream` (a cudaStream_t) for all subsequent work; NULL = the ctx's own stream. */
 bal_status bal_set_stream(bal_ctx* ctx, void* cuda_stream);
@@ -109,7 +153,8 @@ bal_status bal_set_stream(bal_ctx* ctx, void* cuda_stream);
  * Newton-PCG primal solve of §4.  x_t, v_t: device [3N]; x_next: device [3N];
  * v_next: device [3N] or NULL (v_{t+1} = (x_{t+1}-x_t)/h, eq:int:x).  stats may be NULL.
  * Errors: BAL_E_INFEASIBLE (input distance <= 0), BAL_E_NOT_CONVERGED (x_next = last accepted
- * iterate, still intersection-free), BAL_E_NAN, BAL_E_CUDA, BAL_E_OOM. */
+ * iterate, still intersection-free), BAL_E_NAN (sigma^0 or ||e^l|| not finite; x_next = last
+ * accepted iterate), BAL_E_CUDA, BAL_E_OOM. */
 bal_status bal_step(bal_ctx* ctx, const double* x_t, const double* v_t, double* x_next,
                     double* v_next, bal_step_stats* stats);
 
@@ -261,6 +306,24 @@ bal_status bal_spmv_counters(const bal_ctx* ctx, double* out);
 bal_status bal_partition_rows(int32_t n, const int64_t* row_cost, int32_t world, int32_t* bounds);
 int32_t bal_ghost_columns(int32_t n, const int32_t* row_ptr, const int32_t* col, int32_t r0, int32_t r1,
                           int32_t* out, int32_t cap);
+
+/* bal_halo_plan: the boundary-only halo of `rank` for the symmetric block pattern (row_ptr[n+1],
+ * col; both triangles) under the partition bounds[world+1]: per peer m, the owned rows whose
+ * values m needs (send_ptr[m] .. send_ptr[m+1] into send_idx, ascending) and the ghost rows owned
+ * by m (recv_ptr / recv_idx, ascending).  send_ptr / recv_ptr are [world+1]; at most cap entries
+ * are written to each of send_idx / recv_idx (either may be NULL).  Returns max(#send, #recv), or
+ * BAL_E_INVALID_ARG (< 0).  HOST arrays, no CUDA calls.
+ * bal_halo_pack / bal_halo_unpack: the pack (buf[3k+c] = v[3 idx[k]+c]) and unpack (v[3 idx[k]+c]
+ * = buf[3k+c]) of the halo exchange, on HOST arrays (the device kernels use the same routine). */
+int32_t bal_halo_plan(int32_t n, const int32_t* row_ptr, const int32_t* col, int32_t world, const int32_t* bounds,
+                      int32_t rank, int32_t* send_ptr, int32_t* send_idx, int32_t* recv_ptr, int32_t* recv_idx,
+                      int32_t cap);
+bal_status bal_halo_pack(int32_t count, const int32_t* idx, const double* v, double* buf);
+bal_status bal_halo_unpack(int32_t count, const int32_t* idx, const double* buf, double* v);
+
+/* Test surface: y = A v for block rows [r0, r1) only (kSymR-aligned r0; r1 aligned or N); rows
+ * outside are not written.  v, y device [3N]. */
+bal_status bal_spmv_rows(bal_ctx* ctx, int32_t r0, int32_t r1, const double* v, double* y);
 
 /* Counters of kernels launched by the library since ctx creation (bench's gpu_launches). */
 int64_t bal_kernel_launches(const bal_ctx* ctx);

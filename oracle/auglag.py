@@ -28,10 +28,13 @@ def sigma_ls(gb, gE):
     return -float(np.dot(gb, gE)) / bb
 
 
-def sigma_schedule(sigma, sigma0, dmin_new, dhat):
-    """sigma <- max(1.2 sigma, 100 sigma0) if min d(x^{l+1}) < 1e-2 dhat (Alg. 1 lines 15-16, Q8)."""
+def sigma_schedule(sigma, sigma0, dmin_new, dhat, cap=False, use_min=False):
+    """sigma <- max(1.2 sigma, 100 sigma0) if min d(x^{l+1}) < 1e-2 dhat (Alg. 1 lines 15-16, Q8).
+    cap=True: the NEXT-1 sigma-cap reading, an overall ceiling of 1e8 sigma0.
+    use_min=True: min(1.2 sigma, 100 sigma0), capped growth (the SURVEY Q8 alternative)."""
     if dmin_new < 1e-2 * dhat:
-        return max(1.2 * sigma, 100.0 * sigma0)
+        s = min(1.2 * sigma, 100.0 * sigma0) if use_min else max(1.2 * sigma, 100.0 * sigma0)
+        return min(s, 1e8 * sigma0) if cap else s
     return sigma
 
 

@@ -35,10 +35,18 @@ LS_ROUND = 8.0 * 2.0 ** -53
 
 FLAG_NO_WARMSTART = 1
 FLAG_NO_AUGLAG = 2
+FLAG_SIGMA_CAP = 8  # NEXT-1: sigma ceiling 1e8 sigma0 (the GPU's BAL_SIGMA_CAP)
+FLAG_SIGMA_MIN = 16  # min(1.2 sigma, 100 sigma0) reading of Alg. 1 line 16 (the GPU's BAL_SIGMA_MIN)
+FLAG_FRICTION_NO_FREEZE = 32  # literal per-iteration anchors (disables R-FRIC1)
+FREEZE_WINDOW = 10  # R-FRIC1 window (the GPU's kFreezeWindow)
 
 
 class NotConverged(RuntimeError):
     pass
+
+
+class NonFinite(RuntimeError):
+    """sigma^0 or ||e^l|| is not finite (the GPU's BAL_E_NAN)."""
 
 
 def _coo_add(rows, cols, vals, ids, H):
@@ -218,8 +226,10 @@ class Oracle:
         gE[fd] = 0.0
         gb[fd] = 0.0
         floor = float(np.mean(m.mass[self.free])) / (self.h * self.h)
-        s_ls = sigma_ls(gb, gE)
-        return floor if s_ls is None else max(s_ls, floor)
+        with np.errstate(over="ignore", invalid="ignore"):
+            s_ls = sigma_ls(gb, gE)
+        # a non-finite least-squares value (overflowing ||g_b||^2) falls back to the floor (Q7)
+        return floor if (s_ls is None or not np.isfinite(s_ls)) else max(s_ls, floor)
 
     # ---------------------------------------------------------------------- step
     def step(self, x_t, v_t, trace=None):
@@ -238,9 +248,12 @@ class Oracle:
         if len(d) and d.min() <= 0:
             raise ValueError("infeasible input: surface distance <= 0")
         sig0 = self.sigma0(x, st, keys)
+        if not (np.isfinite(sig0) and sig0 > 0.0):
+            raise NonFinite("sigma0 is not a positive finite number")
         st["sigma"] = sig0
         dmin_prev = np.inf
         e0 = None
+        emin, frozen = [], False
         stats = dict(newton=0, pcg=0, ws=0, max_constraints=0)
         converged = False
         for l in range(int(p["max_newton"])):
@@ -261,16 +274,26 @@ class Oracle:
                 st["ap_keys"], st["ap_mu"], st["ap_s"] = newk, mu_new, s_new
                 rebuilt = True
             dmin_prev = dmin
-            fr = self.friction_anchors(x, st, keys)
-            if fr is not None:
-                st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"] = fr
-            else:
-                st["fr_keys"] = None
+            if not frozen:  # friction anchors at x^l, unless frozen (R-FRIC1)
+                fr = self.friction_anchors(x, st, keys)
+                if fr is not None:
+                    st["fr_keys"], st["fr_G"], st["fr_n"], st["fr_lam"] = fr
+                else:
+                    st["fr_keys"] = None
             asm = self.assemble(x, st, keys)
             e = asm["grad"]
             en = float(np.linalg.norm(e))
+            if not np.isfinite(en):
+                raise NonFinite("||e|| is not finite")
             if e0 is None:
                 e0 = en
+            # R-FRIC1: the per-iteration anchor update is a fixed-point iteration;
+            # once the best ||e|| has not halved over FREEZE_WINDOW iterations the anchors are frozen for
+            # the rest of the step (IPC's semi-implicit friction, convergent)
+            emin.append(en if not emin else min(emin[-1], en))
+            if (not frozen and not (self.flags & FLAG_FRICTION_NO_FREEZE) and float(p["chi"]) > 0.0
+                    and l >= FREEZE_WINDOW and emin[l] > 0.5 * emin[l - FREEZE_WINDOW]):
+                frozen = True
             if e0 == 0.0:
                 converged = True
                 break
@@ -288,7 +311,8 @@ class Oracle:
             while True:
                 dirn = pst.x.copy()
                 safeguard = False
-                if float(dirn @ e) >= 0.0:
+                # Q38 descent safeguard; a NaN dot product (PCG stopped on NaN) also falls back
+                if not (float(dirn @ e) < 0.0):
                     dirn = -la.apply_block(Dinv, e)
                     safeguard = True
                 P = dirn.reshape(-1, 3)
@@ -299,8 +323,10 @@ class Oracle:
                 halvings = 0
                 while alpha >= float(p["alpha_min"]):
                     L1, n1, S1 = self.energy(x + alpha * P, st, cpt, cee)
-                    # R-LS1: accept when L does not increase beyond its FP64 evaluation error
-                    if n1 <= int(p["max_constraints"]) and L1 <= L0 + LS_ROUND * max(S0, S1):
+                    # R-LS1: accept when L does not increase beyond its FP64 evaluation error; an
+                    # infeasible trial (J <= 0, d <= 0, NaN) has L = +inf and is never accepted
+                    if (n1 <= int(p["max_constraints"]) and np.isfinite(L1)
+                            and L1 <= L0 + LS_ROUND * max(S0, S1)):
                         break
                     alpha *= 0.5
                     halvings += 1
@@ -336,7 +362,9 @@ class Oracle:
             # sigma schedule (lines 15-16)
             if not (self.flags & FLAG_NO_AUGLAG):
                 _k2, d2 = cm.constraint_set(x_new, cpt, cee, dhat)
-                st["sigma"] = sigma_schedule(st["sigma"], sig0, float(d2.min()) if len(d2) else np.inf, dhat)
+                st["sigma"] = sigma_schedule(st["sigma"], sig0, float(d2.min()) if len(d2) else np.inf, dhat,
+                                             cap=bool(self.flags & FLAG_SIGMA_CAP),
+                                             use_min=bool(self.flags & FLAG_SIGMA_MIN))
             x = x_new
         if not converged:
             raise NotConverged("Newton iteration cap reached")

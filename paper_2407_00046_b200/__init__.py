@@ -13,11 +13,14 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (BAL_FRICTION_LAGGED, BAL_NO_AUGLAG, BAL_NO_WARMSTART, STATUS, bal_bsr_host, bal_contact_state, bal_material,
-                   bal_mesh, bal_params, bal_pcg_opts, bal_pcg_stats, bal_step_stats, bal_system_view)
+from ._lib import (BAL_FRICTION_LAGGED, BAL_FRICTION_NO_FREEZE, BAL_NO_AUGLAG, BAL_NO_WARMSTART, BAL_SIGMA_CAP,
+                   BAL_SIGMA_MIN, STATUS, bal_bsr_host, bal_contact_state, bal_dist, bal_material, bal_mesh,
+                   bal_params, bal_pcg_opts, bal_pcg_stats, bal_step_stats, bal_system_view)
 
 __all__ = ["BalError", "BalCtx", "bal_init", "bal_step", "bal_step_host", "bal_assemble", "bal_spmv", "bal_pcg",
-           "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG", "BAL_FRICTION_LAGGED", "lib_path"]
+           "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "bal_nccl_unique_id", "bal_dist_info", "bal_spmv_rows",
+           "bal_halo_plan", "bal_halo_pack", "bal_halo_unpack", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG",
+           "BAL_FRICTION_LAGGED", "BAL_SIGMA_CAP", "BAL_SIGMA_MIN", "BAL_FRICTION_NO_FREEZE", "lib_path"]
 
 lib_path = _lib.LIB_PATH
 
@@ -34,18 +37,32 @@ def _check(ctx, st):
         raise BalError(st, msg.decode() if msg else "")
 
 
-def _dptr(t):
-    """Device pointer of a contiguous float64/int32 CUDA tensor (or None)."""
+def _dptr(t, numel=None, ctx=None):
+    """Device pointer of a contiguous float64 CUDA tensor (or None); checks dtype, size and device
+    so that no kernel reads or writes out of bounds through a mismatched tensor."""
     if t is None:
         return None
+    import torch
     if not t.is_cuda or not t.is_contiguous():
         raise ValueError("expected a contiguous CUDA tensor")
+    if t.dtype != torch.float64:
+        raise ValueError(f"expected a float64 tensor, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"expected {numel} elements, got {t.numel()}")
+    if ctx is not None and t.device.index != ctx.device:
+        raise ValueError(f"tensor on cuda:{t.device.index}, context on cuda:{ctx.device}")
     return C.c_void_p(t.data_ptr())
 
 
+def _vecs(ctx, *ts):
+    """Device pointers of [3N] float64 tensors of ctx's device (None passes through)."""
+    return [_dptr(t, 3 * ctx.n_nodes, ctx) for t in ts]
+
+
 class BalCtx:
-    def __init__(self, handle, scene):
+    def __init__(self, handle, scene, device=0):
         self.handle = handle
+        self.device = device
         self.n_nodes = int(len(scene["rest_x"]))
         self.n_tets = int(len(scene["tets"]))
         self._keep = []
@@ -82,8 +99,20 @@ def make_params(p, flags=0):
     return prm
 
 
-def bal_init(scene, device=0, flags=0, params=None):
-    """bal_init(mesh, materials, params, device) from a ``scenes`` dict."""
+def bal_nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it)."""
+    buf = (C.c_uint8 * 128)()
+    st = _lib.lib.bal_nccl_unique_id(buf)
+    if st != 0:
+        raise BalError(st, "bal_nccl_unique_id")
+    return bytes(buf)
+
+
+def bal_init(scene, device=0, flags=0, params=None, rank=0, world=1, nccl_id=None, host_transport=None):
+    """bal_init(mesh, materials, params, dist) from a ``scenes`` dict.  world > 1 (or nccl_id /
+    host_transport given) selects the partitioned solve: nccl_id = bal_nccl_unique_id() of rank 0;
+    host_transport = (allreduce(np.ndarray) in place, exchange(send, send_counts, recv_counts) ->
+    recv) Python callables (tests)."""
     x = np.ascontiguousarray(scene["rest_x"], np.float64).ravel()
     tets = np.ascontiguousarray(scene["tets"], np.int32).ravel()
     fixed = np.ascontiguousarray(scene["node_fixed"], np.uint8)
@@ -101,11 +130,45 @@ def bal_init(scene, device=0, flags=0, params=None):
     m.obstacle_tris = _lib.ptr(ob, C.c_int32)
     ma = (bal_material * len(mats))(*[bal_material(*row) for row in mats])
     prm = make_params(params or scene["params"], flags)
+    d = bal_dist()
+    d.rank, d.world, d.device = int(rank), int(world), int(device)
+    keep = []
+    if nccl_id is not None:
+        idb = C.create_string_buffer(bytes(nccl_id), 128)
+        keep.append(idb)
+        d.nccl_unique_id = C.cast(idb, C.c_void_p)
+    if host_transport is not None:
+        ar, ex = host_transport
+
+        def _ar(buf, n, _u):
+            try:
+                a = np.ctypeslib.as_array(buf, shape=(n,))
+                a[:] = ar(a.copy())
+                return 0
+            except Exception:  # noqa: BLE001  (reported to the library as a transport failure)
+                return 1
+
+        def _ex(send, scnt, recv, rcnt, _u):
+            try:
+                sc = np.ctypeslib.as_array(scnt, shape=(world,)).copy()
+                rc = np.ctypeslib.as_array(rcnt, shape=(world,)).copy()
+                s_ = np.ctypeslib.as_array(send, shape=(max(int(sc.sum()), 1),))[:int(sc.sum())].copy()
+                r_ = ex(s_, sc, rc)
+                if int(rc.sum()):
+                    np.ctypeslib.as_array(recv, shape=(int(rc.sum()),))[:] = r_
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        f1, f2 = _lib.HOST_ALLREDUCE(_ar), _lib.HOST_EXCHANGE(_ex)
+        keep += [f1, f2]
+        d.host_allreduce, d.host_exchange = f1, f2
     h = C.c_void_p()
-    st = _lib.lib.bal_init(C.byref(m), ma, len(mats), C.byref(prm), device, C.byref(h))
+    st = _lib.lib.bal_init(C.byref(m), ma, len(mats), C.byref(prm), C.byref(d), C.byref(h))
     if st != 0:
         raise BalError(st, _lib.lib.bal_last_error(None).decode())
-    ctx = BalCtx(h, scene)
+    ctx = BalCtx(h, scene, device)
+    ctx._keep = keep
     try:  # order library work after torch's work on this device (device tensors come from torch)
         import torch
         if torch.cuda.is_available():
@@ -128,13 +191,13 @@ def bal_set_stream(ctx, stream):
 def bal_step(ctx, x_t, v_t, x_next, v_next=None):
     """One time step on device tensors; returns the stats dict."""
     s = bal_step_stats()
-    _check(ctx, _lib.lib.bal_step(ctx.handle, _dptr(x_t), _dptr(v_t), _dptr(x_next), _dptr(v_next), C.byref(s)))
+    _check(ctx, _lib.lib.bal_step(ctx.handle, *_vecs(ctx, x_t, v_t, x_next, v_next), C.byref(s)))
     return {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
 
 
 def bal_frame_begin(ctx, x_t, v_t):
     """Start a time step (setup of Alg. 1) on device tensors; advance it with bal_frame_iterate."""
-    _check(ctx, _lib.lib.bal_frame_begin(ctx.handle, _dptr(x_t), _dptr(v_t)))
+    _check(ctx, _lib.lib.bal_frame_begin(ctx.handle, *_vecs(ctx, x_t, v_t)))
 
 
 def bal_frame_iterate(ctx, max_iters):
@@ -148,7 +211,7 @@ def bal_frame_finish(ctx, x_next=None, v_next=None, allow_unconverged=False):
     """Write x_{t+1}, v_{t+1} of the frame in progress; returns the stats dict.  Raises BalError on
     BAL_E_NOT_CONVERGED unless allow_unconverged (x_next is the last accepted iterate either way)."""
     s = bal_step_stats()
-    st = _lib.lib.bal_frame_finish(ctx.handle, _dptr(x_next), _dptr(v_next), C.byref(s))
+    st = _lib.lib.bal_frame_finish(ctx.handle, *_vecs(ctx, x_next, v_next), C.byref(s))
     out = {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
     out["converged"] = st == 0
     if st == -4 and allow_unconverged:
@@ -245,7 +308,7 @@ def bal_assemble(ctx, x, active_keys=(), aprime_keys=(), aprime_mu=(), aprime_s=
         keep.append(yy)
         cs.y = _lib.ptr(yy, C.c_double)
     v = bal_system_view()
-    _check(ctx, _lib.lib.bal_assemble(ctx.handle, _dptr(x), C.byref(cs), C.byref(v)))
+    _check(ctx, _lib.lib.bal_assemble(ctx.handle, *_vecs(ctx, x), C.byref(cs), C.byref(v)))
     N = v.n_nodes
 
     def view(p, n, dtype):
@@ -287,7 +350,7 @@ def _wrap(p, n, dtype, device):
 
 
 def bal_spmv(ctx, v, y):
-    _check(ctx, _lib.lib.bal_spmv(ctx.handle, _dptr(v), _dptr(y)))
+    _check(ctx, _lib.lib.bal_spmv(ctx.handle, *_vecs(ctx, v, y)))
 
 
 def bal_pcg(ctx, rhs, x0, x_out, warm_start=None, rel_tol=None, stall_window=None, max_iters=None,
@@ -300,7 +363,7 @@ def bal_pcg(ctx, rhs, x0, x_out, warm_start=None, rel_tol=None, stall_window=Non
     o.ws_rel_tol = 1e-2 if ws_rel_tol is None else ws_rel_tol
     o.ws_max_iters = 100 if ws_max_iters is None else ws_max_iters
     s = bal_pcg_stats()
-    _check(ctx, _lib.lib.bal_pcg(ctx.handle, _dptr(rhs), _dptr(x0), _dptr(x_out), C.byref(o), C.byref(s)))
+    _check(ctx, _lib.lib.bal_pcg(ctx.handle, *_vecs(ctx, rhs, x0, x_out), C.byref(o), C.byref(s)))
     return {f: getattr(s, f) for f, _ in bal_pcg_stats._fields_}
 
 
@@ -325,6 +388,58 @@ def bal_bench_spmv(ctx, iters):
     us = C.c_double()
     _check(ctx, _lib.lib.bal_bench_spmv(ctx.handle, iters, C.byref(us)))
     return us.value
+
+
+def bal_dist_info(ctx):
+    """(r0, r1, halo_send, halo_recv): owned block rows and the last solve's halo sizes."""
+    r0, r1 = C.c_int32(), C.c_int32()
+    hs, hr = C.c_int64(), C.c_int64()
+    _check(ctx, _lib.lib.bal_dist_info(ctx.handle, C.byref(r0), C.byref(r1), C.byref(hs), C.byref(hr)))
+    return r0.value, r1.value, hs.value, hr.value
+
+
+def bal_spmv_rows(ctx, r0, r1, v, y):
+    n3 = 3 * ctx.n_nodes
+    _check(ctx, _lib.lib.bal_spmv_rows(ctx.handle, int(r0), int(r1), _dptr(v, n3, ctx), _dptr(y, n3, ctx)))
+
+
+def bal_halo_plan(row_ptr, col, bounds, rank):
+    """Halo plan of `rank` (host): (send_ptr, send_idx, recv_ptr, recv_idx)."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    cl = np.ascontiguousarray(col, np.int32)
+    b = np.ascontiguousarray(bounds, np.int32)
+    world = len(b) - 1
+    sp_ = np.zeros(world + 1, np.int32)
+    rpp = np.zeros(world + 1, np.int32)
+    n = len(rp) - 1
+    m = _lib.lib.bal_halo_plan(n, _lib.ptr(rp, C.c_int32), _lib.ptr(cl, C.c_int32), world, _lib.ptr(b, C.c_int32),
+                               int(rank), _lib.ptr(sp_, C.c_int32), None, _lib.ptr(rpp, C.c_int32), None, 0)
+    if m < 0:
+        raise BalError(m, "bal_halo_plan")
+    si = np.zeros(max(m, 1), np.int32)
+    ri = np.zeros(max(m, 1), np.int32)
+    _lib.lib.bal_halo_plan(n, _lib.ptr(rp, C.c_int32), _lib.ptr(cl, C.c_int32), world, _lib.ptr(b, C.c_int32),
+                           int(rank), _lib.ptr(sp_, C.c_int32), _lib.ptr(si, C.c_int32), _lib.ptr(rpp, C.c_int32),
+                           _lib.ptr(ri, C.c_int32), m)
+    return sp_, si[:sp_[-1]], rpp, ri[:rpp[-1]]
+
+
+def bal_halo_pack(idx, v):
+    idx = np.ascontiguousarray(idx, np.int32)
+    v = np.ascontiguousarray(v, np.float64).ravel()
+    buf = np.zeros(3 * max(len(idx), 1))
+    _check(None, _lib.lib.bal_halo_pack(len(idx), _lib.ptr(idx, C.c_int32), _lib.ptr(v, C.c_double),
+                                        _lib.ptr(buf, C.c_double)))
+    return buf[:3 * len(idx)]
+
+
+def bal_halo_unpack(idx, buf, v):
+    """In place: v[3 idx[k] + c] = buf[3k + c]."""
+    idx = np.ascontiguousarray(idx, np.int32)
+    buf = np.ascontiguousarray(buf, np.float64)
+    _check(None, _lib.lib.bal_halo_unpack(len(idx), _lib.ptr(idx, C.c_int32), _lib.ptr(buf, C.c_double),
+                                          _lib.ptr(v, C.c_double)))
+    return v
 
 
 def bal_partition_rows(row_cost, world):

@@ -26,6 +26,9 @@ STATUS = {0: "OK", -1: "INVALID_ARG", -2: "BAD_MESH", -3: "INFEASIBLE", -4: "NOT
 BAL_NO_WARMSTART = 1
 BAL_NO_AUGLAG = 2
 BAL_FRICTION_LAGGED = 4
+BAL_SIGMA_CAP = 8
+BAL_SIGMA_MIN = 16
+BAL_FRICTION_NO_FREEZE = 32
 
 
 class bal_mesh(C.Structure):
@@ -82,6 +85,15 @@ class bal_pcg_stats(C.Structure):
                 ("n_groups", C.c_int32), ("rel_residual", C.c_double)]
 
 
+HOST_ALLREDUCE = C.CFUNCTYPE(C.c_int32, c_double_p, C.c_int32, C.c_void_p)
+HOST_EXCHANGE = C.CFUNCTYPE(C.c_int32, c_double_p, c_int_p, c_double_p, c_int_p, C.c_void_p)
+
+
+class bal_dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("host_allreduce", HOST_ALLREDUCE), ("host_exchange", HOST_EXCHANGE), ("user", C.c_void_p)]
+
+
 class bal_bsr_host(C.Structure):
     _fields_ = [("n_nodes", C.c_int32), ("nnzb", C.c_int32), ("row_ptr", c_int_p), ("col", c_int_p),
                 ("val", c_double_p), ("group", c_int_p)]
@@ -89,7 +101,14 @@ class bal_bsr_host(C.Structure):
 
 _sig = {
     "bal_init": (C.c_int, [C.POINTER(bal_mesh), C.POINTER(bal_material), C.c_int32, C.POINTER(bal_params),
-                           C.c_int32, C.POINTER(C.c_void_p)]),
+                           C.POINTER(bal_dist), C.POINTER(C.c_void_p)]),
+    "bal_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "bal_dist_info": (C.c_int, [C.c_void_p, c_int_p, c_int_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "bal_halo_plan": (C.c_int32, [C.c_int32, c_int_p, c_int_p, C.c_int32, c_int_p, C.c_int32, c_int_p, c_int_p,
+                                  c_int_p, c_int_p, C.c_int32]),
+    "bal_halo_pack": (C.c_int, [C.c_int32, c_int_p, c_double_p, c_double_p]),
+    "bal_halo_unpack": (C.c_int, [C.c_int32, c_int_p, c_double_p, c_double_p]),
+    "bal_spmv_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "bal_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "bal_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_step_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p,

@@ -17,9 +17,23 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libbal.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dirs():
+    """NCCL of the torch install (the libnccl.so.2 torch loads), else the system one."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []):
+        inc, lib = os.path.join(base, "nccl", "include"), os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+NCCL_INC, NCCL_LIB = _nccl_dirs()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
-         "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC] + os.environ.get("BAL_NVCC_EXTRA", "").split()
+         "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC, "-I" + NCCL_INC] + os.environ.get("BAL_NVCC_EXTRA", "").split()
 
 
 def _sources():
@@ -68,7 +82,8 @@ def build(verbose=False, clean=False):
         raise RuntimeError("nvcc failed:\n" + "\n".join(errors))
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", LIB, *objs, "-lcudart",
+               "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr + r.stdout)

@@ -10,14 +10,66 @@
 
 using namespace bal;
 
+void SymTilesDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& urow,
+                        const std::vector<int>& upos, const std::vector<int>& ucol, cudaStream_t st) {
+  std::vector<int> mirp(N + 1, 0), morp(N + 1, 0), mopos, mocol;
+  std::vector<unsigned short> miloc;
+  cap = 0;
+  ocap = 0;
+  for (int r0 = 0; r0 < N; r0 += kSymR) {
+    const int r1 = std::min(N, r0 + kSymR);
+    const int s0 = lrow[r0];
+    cap = std::max(cap, lrow[r1] - s0);
+    for (int j = r0; j < r1; ++j) {
+      for (int e = urow[j]; e < urow[j + 1]; ++e) {
+        if (ucol[e] < r1) {
+          miloc.push_back((unsigned short)(upos[e] - s0));
+        } else {
+          mopos.push_back(upos[e]);
+          mocol.push_back(ucol[e]);
+        }
+      }
+      mirp[j + 1] = (int)miloc.size();
+      morp[j + 1] = (int)mopos.size();
+    }
+    ocap = std::max(ocap, morp[r1] - morp[r0]);
+  }
+  if (cap >= 65536) {  // local indices are 16-bit: fall back to the generic kernel
+    ready = false;
+    return;
+  }
+  mi_rp.upload(mirp.data(), mirp.size(), st);
+  mo_rp.upload(morp.data(), morp.size(), st);
+  mi_loc.upload(miloc.data(), std::max<size_t>(miloc.size(), 1), st);
+  mo_pos.upload(mopos.data(), std::max<size_t>(mopos.size(), 1), st);
+  mo_col.upload(mocol.data(), std::max<size_t>(mocol.size(), 1), st);
+  ready = true;
+}
+
+void SymTilesDev::wire(Bsr& b) const {
+  if (!ready) return;
+  b.mi_row_ptr = mi_rp.ptr;
+  b.mi_loc = mi_loc.ptr;
+  b.mo_row_ptr = mo_rp.ptr;
+  b.mo_pos = mo_pos.ptr;
+  b.mo_col = mo_col.ptr;
+  b.tcap = cap;
+  b.tocap = ocap;
+}
+
 bal::Bsr bal_ctx::static_bsr() const {
   Bsr b;
   b.n = N;
   if (loaded_bsr) {
-    b.nnzb = lb_nnzb;
-    b.row_ptr = lb_row_ptr.ptr;
-    b.col = lb_col.ptr;
-    b.val = lb_val.ptr;
+    b.nnzb = lb_nl;
+    b.row_ptr = lb_lrow.ptr;
+    b.col = lb_lcol.ptr;
+    b.val = lb_lval.ptr;
+    b.m_row_ptr = lb_urow.ptr;
+    b.m_pos = lb_upos.ptr;
+    b.m_col = lb_ucol.ptr;
+    b.nmirror = lb_nu;
+    lb_tiles.wire(b);
   } else if (sp_sym) {
     b.nnzb = sp.nl;
     b.row_ptr = sp.l_row_ptr;
@@ -27,6 +79,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.m_pos = sp.u_pos;
     b.m_col = sp.u_col;
     b.nmirror = sp.nu;
+    sp_tiles.wire(b);
   } else {
     b.nnzb = sp.nnzb;
     b.row_ptr = sp.row_ptr;
@@ -73,6 +126,12 @@ bal_status guard(bal_ctx* c, F&& f) {
   } catch (const ArgError& e) {
     if (c) c->err = e.what();
     return BAL_E_INVALID_ARG;
+  } catch (const std::invalid_argument& e) {
+    if (c) c->err = e.what();
+    return BAL_E_INVALID_ARG;
+  } catch (const NcclError& e) {
+    if (c) c->err = e.what();
+    return BAL_E_NCCL;
   } catch (const std::exception& e) {
     if (c) c->err = e.what();
     return BAL_E_CUDA;
@@ -294,6 +353,8 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->tris.upload(trisf.data(), trisf.size(), st);
   c->edges.upload(edgesf.data(), edgesf.size(), st);
   c->sverts.upload(sv.data(), sv.size(), st);
+  c->dist.adj_ptr = row_ptr;  // host copy of the static pattern for the halo plan (kept if distributed)
+  c->dist.adj_col = col;
   c->sp_row_ptr.upload(row_ptr.data(), row_ptr.size(), st);
   c->sp_col.upload(col.data(), col.size(), st);
   c->sp_slot_row.upload(slot_row.data(), slot_row.size(), st);
@@ -334,7 +395,9 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     c->sp.nu = (int)ucol.size();
     c->sp_lpos.upload(lpos.data(), lpos.size(), st);
     c->sp_lrow.upload(lrow.data(), lrow.size(), st);
-    c->sp_lcol.upload(lcol.data(), std::max<size_t>(lcol.size(), 1), st);
+    lcol.resize(lcol.size() + 8, 0);  // 16-byte slack: the tile bulk copies round the range up
+    c->sp_lcol.upload(lcol.data(), lcol.size(), st);
+    lcol.resize(lcol.size() - 8);
     c->sp_urow.upload(urow.data(), urow.size(), st);
     c->sp_upos.upload(upos.data(), std::max<size_t>(upos.size(), 1), st);
     c->sp_ucol.upload(ucol.data(), std::max<size_t>(ucol.size(), 1), st);
@@ -345,12 +408,16 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     c->sp.u_pos = c->sp_upos.ptr;
     c->sp.u_col = c->sp_ucol.ptr;
     c->sp_sym = spmv_symmetric_enabled();
-    if (c->sp_sym) c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1));
+    if (c->sp_sym) {
+      c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1) + 2);  // + 16 B slack for the bulk copies
+      if (getenv("BAL_SPMV_GENERIC") == nullptr) c->sp_tiles.build(N, lrow, urow, upos, ucol, st);
+    }
     for (int r0 = 0; r0 < N; r0 += kSpmvTileRows)
       c->sp.tile_cap_full = std::max(c->sp.tile_cap_full,
                                      row_ptr[std::min(N, r0 + kSpmvTileRows)] - row_ptr[r0]);
     spmv_init_grids();
     spmv_prepare(c->static_bsr());
+    spmv_sym_prepare(c->static_bsr());
   }
   c->sval.reserve(9 * (size_t)nnzb);
   c->stage_e.reserve(90 * (size_t)std::max(T, 1));
@@ -422,10 +489,14 @@ static thread_local std::string g_init_err;
 extern "C" {
 
 bal_status bal_init(const bal_mesh* mesh, const bal_material* materials, int32_t n_materials,
-                    const bal_params* params, int32_t device, bal_ctx** out) {
+                    const bal_params* params, const bal_dist* dist, bal_ctx** out) {
   if (!out) return BAL_E_INVALID_ARG;
   *out = nullptr;
   if (!mesh || !materials || n_materials <= 0 || !params) return BAL_E_INVALID_ARG;
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world ||
+               ((dist->host_allreduce == nullptr) != (dist->host_exchange == nullptr))))
+    return BAL_E_INVALID_ARG;
+  const int device = dist ? dist->device : 0;
   bal_ctx* c = new bal_ctx();
   c->device = device;
   c->prm = *params;
@@ -440,6 +511,13 @@ bal_status bal_init(const bal_mesh* mesh, const bal_material* materials, int32_t
     c->st = c->own_stream;
     if (!(c->prm.h > 0) || !(c->prm.dhat > 0)) throw ArgError("bal_init: h and dhat must be > 0");
     precompute(c, mesh, materials, n_materials);
+    if (dist) dist_init(c, dist);
+    if (!c->dist.active) {
+      c->dist.adj_ptr.clear();
+      c->dist.adj_ptr.shrink_to_fit();
+      c->dist.adj_col.clear();
+      c->dist.adj_col.shrink_to_fit();
+    }
     return BAL_OK;
   });
   if (s != BAL_OK) {
@@ -522,6 +600,20 @@ bal_status bal_spmv(bal_ctx* c, const double* v, double* y) {
   });
 }
 
+bal_status bal_spmv_rows(bal_ctx* c, int32_t r0, int32_t r1, const double* v, double* y) {
+  if (!c || !v || !y || r0 < 0 || r1 < r0 || r1 > c->N) return BAL_E_INVALID_ARG;
+  if (r0 % kSymR != 0 || (r1 != c->N && r1 % kSymR != 0)) return BAL_E_INVALID_ARG;
+  return guard(c, [&]() {
+    Bsr S = c->static_bsr();
+    S.r0 = r0;
+    S.r1 = r1;
+    if (r1 > r0) launch_spmv(c->st, S, c->contact_bsr(), v, y);
+    c->launches += 1;
+    CK(cudaStreamSynchronize(c->st));
+    return BAL_OK;
+  });
+}
+
 bal_status bal_pcg(bal_ctx* c, const double* rhs, const double* x0, double* x_out, const bal_pcg_opts* o,
                    bal_pcg_stats* stats) {
   if (!c || !rhs || !x_out) return BAL_E_INVALID_ARG;
@@ -551,6 +643,46 @@ bal_status bal_load_bsr(bal_ctx* c, const bal_bsr_host* b) {
     c->lb_val.upload(b->val, 9 * (size_t)b->nnzb, st);
     c->lb_nnzb = b->nnzb;
     c->loaded_bsr = true;
+    {  // symmetric copy (the SpMV reads the lower triangle; the loaded matrix must be symmetric)
+      const int N = c->N;
+      auto find = [&](int i, int j) {
+        for (int s2 = b->row_ptr[i]; s2 < b->row_ptr[i + 1]; ++s2)
+          if (b->col[s2] == j) return s2;
+        throw ArgError("bal_load_bsr: pattern is not structurally symmetric");
+      };
+      std::vector<int> lpos(b->nnzb, -1), lrow(N + 1, 0), lcol, urow(N + 1, 0), upos, ucol;
+      std::vector<double> lv;
+      for (int i = 0; i < N; ++i) {
+        for (int s2 = b->row_ptr[i]; s2 < b->row_ptr[i + 1]; ++s2)
+          if (b->col[s2] <= i) {
+            lpos[s2] = (int)lcol.size();
+            lcol.push_back(b->col[s2]);
+            lv.insert(lv.end(), b->val + 9 * (size_t)s2, b->val + 9 * (size_t)s2 + 9);
+          }
+        lrow[i + 1] = (int)lcol.size();
+      }
+      for (int i = 0; i < N; ++i) {
+        for (int s2 = b->row_ptr[i]; s2 < b->row_ptr[i + 1]; ++s2)
+          if (b->col[s2] > i) {
+            upos.push_back(lpos[find(b->col[s2], i)]);
+            ucol.push_back(b->col[s2]);
+          }
+        urow[i + 1] = (int)ucol.size();
+      }
+      c->lb_nl = (int)lcol.size();
+      c->lb_nu = (int)ucol.size();
+      lcol.resize(lcol.size() + 8, 0);
+      lv.resize(lv.size() + 2, 0.0);
+      c->lb_lrow.upload(lrow.data(), lrow.size(), st);
+      c->lb_lcol.upload(lcol.data(), lcol.size(), st);
+      c->lb_lval.upload(lv.data(), lv.size(), st);
+      c->lb_urow.upload(urow.data(), urow.size(), st);
+      c->lb_upos.upload(upos.data(), std::max<size_t>(upos.size(), 1), st);
+      c->lb_ucol.upload(ucol.data(), std::max<size_t>(ucol.size(), 1), st);
+      lcol.resize(lcol.size() - 8);
+      if (getenv("BAL_SPMV_GENERIC") == nullptr) c->lb_tiles.build(N, lrow, urow, upos, ucol, st);
+      spmv_sym_prepare(c->static_bsr());
+    }
 
     // diagonal inverse from the loaded blocks (host: test path only)
     std::vector<double> dinv(6 * (size_t)c->N, 0.0);
@@ -629,6 +761,7 @@ void bal_destroy(bal_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   destroy_step_work(c);
+  dist_destroy(c);
   if (c->ev_ready)
     for (cudaEvent_t e : c->ev)
       if (e) cudaEventDestroy(e);

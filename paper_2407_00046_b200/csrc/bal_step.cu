@@ -32,6 +32,9 @@ struct StepWork {
     bool active = false, converged = false;
     int l = 0;
     double sigma = 0, sig0 = 0, dmin = 0, dmin_prev = 0, e0 = -1;
+    // R-FRIC1: history of min ||e|| for the friction-anchor freeze
+    std::vector<double> emin;
+    bool fric_frozen = false;
     bal_step_stats S{};
     std::chrono::steady_clock::time_point t_start;
   } fr;
@@ -210,11 +213,14 @@ struct Energy {
   int count;
   double dmin;
   double S;
+  double part[5];  // elastic, inertia, barrier, AL, friction (BAL_VERBOSE=2 diagnostics)
 };
 
 // R-LS1: the line search accepts L(x + a p) <= L(x) + 8u max(S0, S1), i.e. no increase
 // beyond the FP64 evaluation error of L (S = sum of the magnitudes of its terms).
 constexpr double kLsRound = 8.0 * 1.1102230246251565e-16;
+// R-FRIC1: window of the friction-anchor freeze test
+constexpr int kFreezeWindow = 10;
 
 double host_scalar(bal_ctx* c, const double* dev) {
   double v;
@@ -271,6 +277,11 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
   // magnitude scale of the FP64 evaluation error of L (DESIGN.md R-LS1)
   r.S = std::fabs(hv[1]) + std::fabs(hv[0]) + std::fabs(hv[2]) + hv[7] + std::fabs(hv[6]);
   if (!std::isfinite(r.L)) r.S = INFINITY;
+  r.part[0] = hv[0];
+  r.part[1] = hv[1];
+  r.part[2] = hv[2];
+  r.part[3] = hv[4];
+  r.part[4] = hv[6];
   return r;
 }
 
@@ -335,9 +346,12 @@ double sigma0(bal_ctx* c, StepWork& w, const double* x) {
                                                          c->fixed.ptr, w.gb.ptr);
   c->launches += 6;
   const double bb = norm2(c, w.gb.ptr, 3 * N);
-  if (bb == 0.0) return floor_;
+  if (bb == 0.0 || !std::isfinite(bb)) return floor_;
   const double be = dotp(c, w.gb.ptr, w.gE.ptr, 3 * N);
-  return std::max(-be / bb, floor_);
+  const double s_ls = -be / bb;
+  // a non-finite least-squares value (overflowing ||g_b||^2 of extremely close pairs) falls back to
+  // the floor instead of poisoning the frame (Q7 floor)
+  return std::isfinite(s_ls) ? std::max(s_ls, floor_) : floor_;
 }
 
 void rebuild_aprime(bal_ctx* c, StepWork& w) {
@@ -395,10 +409,11 @@ double ms_since(std::chrono::steady_clock::time_point t0) {
 
 // ---- Alg. 1 split into frame setup / Newton iterations / finish so callers (bench)
 // can advance a frame in slices of Newton iterations; bal_step = begin + iterate(max_newton) + finish.
-static bool verbose_on() {
-  static const bool v = getenv("BAL_VERBOSE") != nullptr;
+static int verbose_level() {
+  static const int v = getenv("BAL_VERBOSE") ? std::max(1, atoi(getenv("BAL_VERBOSE"))) : 0;
   return v;
 }
+static bool verbose_on() { return verbose_level() > 0; }
 static void vmark(bal_ctx* c, std::chrono::steady_clock::time_point& t_mark, const char* what, long long a = -1,
                   long long b = -1) {
   if (!verbose_on()) return;
@@ -438,6 +453,8 @@ void frame_begin(bal_ctx* c, const double* x_t, const double* v_t) {
   t0 = clk::now();
   F.sig0 = sigma0(c, w, w.x.ptr);
   vmark(c, t_mark, "sigma0");
+  if (!std::isfinite(F.sig0) || !(F.sig0 > 0.0))
+    throw StepFail(BAL_E_NAN, "bal_step: sigma0 is not a positive finite number");
   F.S.ms_assembly += ms_since(t0);
   F.sigma = F.sig0;
   F.dmin_prev = INFINITY;
@@ -499,8 +516,9 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
     // friction anchors at x^l; ablation BAL_FRICTION_LAGGED: anchors of the frame's first
     // iterate kept for the whole frame (IPC's lagged, semi-implicit friction)
     const bool lagged = (P.flags & BAL_FRICTION_LAGGED) != 0;
-    if (!lagged || l == 0) c->n_fric = 0;
-    if (P.chi > 0.0 && c->cset.n > 0 && (!lagged || l == 0)) {
+    const bool keep = lagged ? l > 0 : F.fric_frozen;
+    if (!keep) c->n_fric = 0;
+    if (P.chi > 0.0 && c->cset.n > 0 && !keep) {
       const int nc = c->cset.n;
       c->fr_keys.reserve(5 * (size_t)nc);
       c->fr_gam.reserve(4 * (size_t)nc);
@@ -517,7 +535,15 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
     mark("assembly", c->cw.nslots);
     const double en = std::sqrt(norm2(c, c->grad.ptr, 3 * N));
     S.ms_assembly += ms_since(t0);
+    if (!std::isfinite(en)) throw StepFail(BAL_E_NAN, "bal_step: ||e|| is not finite");
     if (e0 < 0) e0 = en;
+    // R-FRIC1: the per-iteration anchor update is a fixed-point iteration; once
+    // the best ||e|| has not halved over kFreezeWindow Newton iterations the anchors are frozen for
+    // the rest of the step (IPC's semi-implicit friction, convergent)
+    F.emin.push_back(F.emin.empty() ? en : std::min(F.emin.back(), en));
+    if (!F.fric_frozen && !(P.flags & BAL_FRICTION_NO_FREEZE) && P.chi > 0.0 && l >= kFreezeWindow &&
+        F.emin[l] > 0.5 * F.emin[l - kFreezeWindow])
+      F.fric_frozen = true;
     if (e0 == 0.0) {
       F.converged = true;
       ++F.l;
@@ -538,7 +564,8 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
     double alpha = 0.0, a_ccd = 1.0;
     t0 = clk::now();
     while (true) {
-      if (dotp(c, w.dir.ptr, c->grad.ptr, 3 * N) >= 0.0) {  // Q38 descent safeguard
+      // Q38 descent safeguard; a NaN dot product (PCG stopped on NaN) also takes the -D^{-1} e fallback
+      if (!(dotp(c, w.dir.ptr, c->grad.ptr, 3 * N) < 0.0)) {
         launch_apply_dinv(st, N, c->dinv.ptr, c->grad.ptr, w.dir.ptr, -1.0);
         safeguard = 1;
       }
@@ -558,7 +585,14 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
         launch_axpy(st, 3 * N, alpha, w.dir.ptr, w.x.ptr, w.trial.ptr);
         E1 = energy(c, w, w.trial.ptr, w.cand_sw, sigma);
         mark("energy", E1.count);
-        if (E1.count <= P.max_constraints && E1.L <= E0.L + kLsRound * std::max(E0.S, E1.S)) {
+        if (verbose_level() >= 2)
+          fprintf(stderr,
+                  "[bal]     ls a=%.3e dL=%.6e  d(el)=%.3e d(in)=%.3e d(bar)=%.3e d(al)=%.3e d(fr)=%.3e dmin=%.3e n=%d\n",
+                  alpha, E1.L - E0.L, E1.part[0] - E0.part[0], E1.part[1] - E0.part[1], E1.part[2] - E0.part[2],
+                  E1.part[3] - E0.part[3], E1.part[4] - E0.part[4], E1.dmin, E1.count);
+        // R-LS1; an infeasible trial (J <= 0, d <= 0, NaN) has L = +inf and is never accepted
+        if (E1.count <= P.max_constraints && std::isfinite(E1.L) &&
+            E1.L <= E0.L + kLsRound * std::max(E0.S, E1.S)) {
           ok = true;
           break;
         }
@@ -609,7 +643,12 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
     }
     if (!no_al) {  // Alg. 1 lines 15-16
       const double dnew = min_d(c, w, w.cs_trial);
-      if (dnew < 1e-2 * dhat) sigma = std::max(1.2 * sigma, 100.0 * sig0);
+      if (dnew < 1e-2 * dhat) {
+        // verbatim max (Q8); BAL_SIGMA_MIN: the capped-growth reading min(1.2 sigma, 100 sigma0)
+        sigma = (P.flags & BAL_SIGMA_MIN) ? std::min(1.2 * sigma, 100.0 * sig0) : std::max(1.2 * sigma, 100.0 * sig0);
+        // NEXT-1 ablation BAL_SIGMA_CAP: overall ceiling 1e8 sigma0 (SPEC S:516 reading of line 16)
+        if (P.flags & BAL_SIGMA_CAP) sigma = std::min(sigma, 1e8 * sig0);
+      }
     }
     std::swap(w.x.ptr, w.trial.ptr);
   }
@@ -665,6 +704,9 @@ bal_status guard_step(bal_ctx* c, F&& f) {
   } catch (const OomError& e) {
     c->err = e.what();
     return BAL_E_OOM;
+  } catch (const NcclError& e) {
+    c->err = e.what();
+    return BAL_E_NCCL;
   } catch (const std::exception& e) {
     c->err = e.what();
     return BAL_E_CUDA;

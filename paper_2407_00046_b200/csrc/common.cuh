@@ -18,6 +18,9 @@ struct CudaError : std::runtime_error {
 struct OomError : std::runtime_error {
   explicit OomError(const std::string& s) : std::runtime_error(s) {}
 };
+struct NcclError : std::runtime_error {
+  explicit NcclError(const std::string& s) : std::runtime_error(s) {}
+};
 
 #define CK(call)                                                                            \
   do {                                                                                      \
@@ -33,6 +36,19 @@ struct OomError : std::runtime_error {
 
 // 148 SMs on B200: grid sizes for grid-stride / reduction kernels are multiples of it.
 constexpr int kSMs = 148;
+// SM count of the current device (MIG / MPS partitions may expose fewer): persistent and
+// cooperative grids are sized from it.
+inline int num_sms() {
+  static int n[64] = {0};
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return kSMs;
+  if (n[d] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = kSMs;
+    n[d] = v;
+  }
+  return n[d];
+}
 constexpr int kRedBlocks = 4 * kSMs;  // fixed reduction grid -> deterministic partial order
 constexpr int kRedThreads = 256;
 

@@ -7,6 +7,38 @@
 #include "assemble.h"
 #include "kernels.h"
 #include "keys.h"
+#include "halo.h"
+
+// Device copy of the TMA-staged symmetric SpMV's per-row mirror split (k_spmv.cu, Bsr::mi_*/mo_*).
+struct SymTilesDev {
+  bal::DevBuf<int> mi_rp, mo_rp, mo_pos, mo_col;
+  bal::DevBuf<unsigned short> mi_loc;
+  int cap = 0, ocap = 0;
+  bool ready = false;
+  // lower CSR (row_ptr lrow[N+1]) + mirror index (urow[N+1], upos/ucol: lower position of (j, i), j)
+  void build(int N, const std::vector<int>& lrow, const std::vector<int>& urow, const std::vector<int>& upos,
+             const std::vector<int>& ucol, cudaStream_t st);
+  void wire(bal::Bsr& b) const;
+};
+
+// Partitioned solve state (pcg_dist.cu).  active = the distributed PCG path is used.
+struct DistState {
+  bool active = false;
+  int rank = 0, world = 1, r0 = 0, r1 = 0;  // owned block rows [r0, r1)
+  std::vector<int32_t> bounds;               // [world+1]
+  void* comm = nullptr;                      // ncclComm_t (nullptr with the host transport)
+  bal_host_allreduce_fn h_allreduce = nullptr;
+  bal_host_exchange_fn h_exchange = nullptr;
+  void* user = nullptr;
+  std::vector<int32_t> adj_ptr, adj_col;  // static symmetric block pattern (host) for the halo plan
+  bal::HaloPlan plan;
+  bal::DevBuf<int> send_idx, recv_idx;
+  bal::DevBuf<double> sbuf, rbuf, red, vec;  // red: [0,256) local sums, [256,512) all-reduced
+  std::vector<double> h_sbuf, h_rbuf, h_red, h_vec;
+  std::vector<int32_t> h_sc, h_rc;  // per-peer counts in doubles (host transport)
+  bal::DevBuf<bal::PcgScal> lscal;  // sink of the owned-rows p^T A p of the SpMV epilogue
+  long long halo_send = 0, halo_recv = 0;
+};
 
 struct bal_ctx {
   int device = 0;
@@ -36,6 +68,7 @@ struct bal_ctx {
   bal::DevBuf<int> sp_lpos, sp_lrow, sp_lcol, sp_urow, sp_upos, sp_ucol;  // symmetric SpMV copy
   bal::DevBuf<double> lval;
   bool sp_sym = false;
+  SymTilesDev sp_tiles;
   // ---- elastic stencils
   bal::DevBuf<double> stage_e, grad_e, lbar_e;
   // ---- contact + friction stencils (friction appended after contact)
@@ -54,6 +87,11 @@ struct bal_ctx {
   bal::DevBuf<int> lb_row_ptr, lb_col;
   bal::DevBuf<double> lb_val;
   int lb_nnzb = 0;
+  // symmetric copy of the loaded system (lower + diagonal blocks, mirror index, tiles)
+  bal::DevBuf<int> lb_lrow, lb_lcol, lb_urow, lb_upos, lb_ucol;
+  bal::DevBuf<double> lb_lval;
+  int lb_nl = 0, lb_nu = 0;
+  SymTilesDev lb_tiles;
   // ---- PCG
   bal::DevBuf<double> pr, pz, pp, pq, px, partials, hist;
   bal::DevBuf<unsigned> counter;
@@ -89,6 +127,8 @@ struct bal_ctx {
     return stat + contact + 48.0 * n;
   }
 
+  DistState dist;
+
   // ---- time-step work (bal_step.cu), allocated on first use
   struct StepWork* sw = nullptr;
   std::vector<double> trace;  // per-Newton-iteration decision trace of the last bal_step
@@ -105,4 +145,10 @@ void compact_groups(bal_ctx* c);
 int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
               int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats);
 void pcg_resume(bal_ctx* c, int extra, double* x_out, bal_pcg_stats* stats);
+// partitioned solve (pcg_dist.cu)
+void dist_init(bal_ctx* c, const bal_dist* d);
+void dist_destroy(bal_ctx* c);
+int pcg_solve_dist(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
+                   int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats);
+void pcg_resume_dist(bal_ctx* c, int extra, double* x_out, bal_pcg_stats* stats);
 }  // namespace bal

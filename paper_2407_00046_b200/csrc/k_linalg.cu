@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "reduce.cuh"
 
 namespace bal {
 
@@ -40,13 +41,14 @@ template <bool DOT, bool MASK>
 __global__ void k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v,
                        double* __restrict__ y, double* partials, unsigned* counter, PcgScal* sc, const GrpScal* gs);
 template <bool DOT, bool MASK>
-static int spmv_grid(int n) {
+static int spmv_grid(const Bsr& S) {
+  const int n = S.row_end() - (S.r0 / kTileRows) * kTileRows;
   static int per_sm = 0;
   if (per_sm == 0) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv<DOT, MASK>, kSpmvThreads, 0));
     per_sm = std::max(per_sm, 1);
   }
-  return std::max(1, std::min(per_sm * kSMs, ceil_div((long long)n, kTileRows)));
+  return std::max(1, std::min(per_sm * num_sms(), ceil_div((long long)n, kTileRows)));
 }
 
 // Tiled, flattened SpMV.  A CTA owns a tile of kTileRows consecutive block rows and walks the
@@ -98,12 +100,12 @@ k_spmv(Bsr S, Bsr C, const int* __restrict__ grp, const double* __restrict__ v, 
   const int n = S.n;
   const int tid = threadIdx.x;
   const unsigned long long pol_first = policy_evict_first(), pol_last = policy_evict_last();
-  const int ntiles = (n + kTileRows - 1) / kTileRows;
+  const int ntiles = (S.row_end() + kTileRows - 1) / kTileRows;
   const int* crp = C.nnzb > 0 ? C.row_ptr : nullptr;
   double dacc = 0.0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int tile = S.r0 / kTileRows + blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int r0 = tile * kTileRows;
-    const int R = min(kTileRows, n - r0);
+    const int R = min(kTileRows, S.row_end() - r0);
     // ---- stage 1: row pointers (3 lists) and row groups
     for (int t = tid; t < 3 * (kTileRows + 1); t += blockDim.x) {
       const int L = t / (kTileRows + 1), k = t - L * (kTileRows + 1);
@@ -369,10 +371,12 @@ static int spmv_sf_grid(const Bsr& S, size_t& smem) {
     smem_at[key] = smem;
   }
   if (per_sm[key] <= 0) return 0;
-  return std::max(1, std::min(per_sm[key] * kSMs, ceil_div((long long)S.n, kTileRows)));
+  return std::max(1, std::min(per_sm[key] * num_sms(), ceil_div((long long)S.n, kTileRows)));
 }
 
-static bool spmv_sf_usable(const Bsr& S) { return !S.m_row_ptr && S.tile_cap_s > 0 && S.tile_cap_s <= 2048; }
+static bool spmv_sf_usable(const Bsr& S) {
+  return !S.m_row_ptr && S.tile_cap_s > 0 && S.tile_cap_s <= 2048 && S.r0 == 0 && S.row_end() == S.n;
+}
 
 void spmv_prepare(const Bsr& S) {  // occupancy / smem attribute outside any stream capture
   if (!spmv_sf_usable(S)) return;
@@ -382,13 +386,16 @@ void spmv_prepare(const Bsr& S) {  // occupancy / smem attribute outside any str
 }
 
 void spmv_init_grids() {  // occupancy queries outside any stream capture (called by bal_init)
-  (void)spmv_grid<false, false>(1);
-  (void)spmv_grid<true, false>(1);
-  (void)spmv_grid<false, true>(1);
+  Bsr one;
+  one.n = 1;
+  (void)spmv_grid<false, false>(one);
+  (void)spmv_grid<true, false>(one);
+  (void)spmv_grid<false, true>(one);
 }
 
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y) {
   if (S.n <= 0) return;
+  if (launch_spmv_sym(st, S, C, v, y, nullptr, nullptr, nullptr)) return;
   if (spmv_sf_usable(S)) {
     size_t sm = 0;
     const int g = spmv_sf_grid<false>(S, sm);
@@ -398,13 +405,14 @@ void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, d
       return;
     }
   }
-  const int blocks = spmv_grid<false, false>(S.n);
+  const int blocks = spmv_grid<false, false>(S);
   k_spmv<false, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, nullptr, nullptr, nullptr, nullptr);
   CK(cudaGetLastError());
 }
 
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* partials,
                      unsigned* counter, PcgScal* sc) {
+  if (launch_spmv_sym(st, S, C, v, y, partials, counter, sc)) return;
   if (spmv_sf_usable(S)) {
     size_t sm = 0;
     const int g = spmv_sf_grid<true>(S, sm);
@@ -414,87 +422,17 @@ void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* 
       return;
     }
   }
-  const int blocks = spmv_grid<true, false>(S.n);
+  const int blocks = spmv_grid<true, false>(S);
   k_spmv<true, false><<<blocks, kSpmvThreads, 0, st>>>(S, C, nullptr, v, y, partials, counter, sc, nullptr);
   CK(cudaGetLastError());
 }
 
 void launch_spmv_masked(cudaStream_t st, const Bsr& S, const Bsr& C, const int* grp, const double* v, double* y,
                         const GrpScal* gs) {
-  const int blocks = spmv_grid<false, true>(S.n);
+  const int blocks = spmv_grid<false, true>(S);
   k_spmv<false, true><<<blocks, kSpmvThreads, 0, st>>>(S, C, grp, v, y, nullptr, nullptr, nullptr, gs);
   CK(cudaGetLastError());
 }
-
-// ---------------------------------------------------------------------------------- vectors
-BAL_D void dinv_apply(const double* __restrict__ dinv, int i, double r0, double r1, double r2, double& z0,
-                      double& z1, double& z2) {
-  const double* m = dinv + 6 * (size_t)i;
-  z0 = m[0] * r0 + m[1] * r1 + m[2] * r2;
-  z1 = m[1] * r0 + m[3] * r1 + m[4] * r2;
-  z2 = m[2] * r0 + m[4] * r1 + m[5] * r2;
-}
-
-// last-block finalisation helper for NQ quantities
-template <int NQ, int NT>
-BAL_D bool last_block_reduce(const double (&loc)[NQ], double* partials, unsigned* counter, double (&tot)[NQ]) {
-  __shared__ double sh[NT / 32];
-  __shared__ bool last;
-  double bs[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) bs[q] = block_sum<NT>(loc[q], sh);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) partials[NQ * blockIdx.x + q] = bs[q];
-    __threadfence();
-    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    double t = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += partials[NQ * i + q];
-    tot[q] = block_sum<NT>(t, sh);
-  }
-  if (threadIdx.x == 0) *counter = 0u;
-  return true;
-}
-
-// App. B stop logic (oracle.linalg.pcg_run order): NaN, converged, stagnation, cap.
-BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
-  const int k = sc->k;
-  const double rn = hist[k];
-  if (!isfinite(rn)) {
-    sc->stop = 3;
-    sc->done = 1;
-    return;
-  }
-  if (rn <= sc->tol * sc->bnorm) {
-    sc->stop = 0;
-    sc->done = 1;
-    return;
-  }
-  // R-PCG1: stagnation = the CG objective (monotone in PCG) decreased by no more than kStallRel of
-  // its total decrease over the last W iterations
-  const int W = sc->window;
-  if (W > 0 && k >= W) {
-    const double* dh = hist + sc->hcap;
-    if (dh[k] - dh[k - W] <= kStallRel * dh[k]) {
-      sc->stop = 1;
-      sc->done = 1;
-      return;
-    }
-  }
-  if (k >= sc->max_iters) {
-    sc->stop = 2;
-    sc->done = 1;
-  }
-}
-
-constexpr int kVecThreads = 256;
-constexpr int kVecBlocks = 4 * kSMs;
 
 __global__ void __launch_bounds__(kVecThreads)
 k_pcg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, const double* __restrict__ dinv,
@@ -675,10 +613,10 @@ int pcg_fused_grid(int n, int* kvariant) {
   if (off) return 0;
   for (int K : {4, 8}) {
     const int per_sm = fused_per_sm(K);
-    const long long cap = (long long)per_sm * kSMs * kVecThreads * K;
+    const long long cap = (long long)per_sm * num_sms() * kVecThreads * K;
     if (per_sm > 0 && n <= cap) {
       if (kvariant) *kvariant = K;
-      return std::min(per_sm * kSMs, std::max(1, ceil_div((long long)n, (long long)kVecThreads * K)));
+      return std::min(per_sm * num_sms(), std::max(1, ceil_div((long long)n, (long long)kVecThreads * K)));
     }
   }
   return 0;
@@ -696,61 +634,6 @@ void launch_pcg_update_fused(cudaStream_t st, int grid, int n, const double* din
 void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc) {
   k_pcg_pupdate<<<kVecBlocks, kVecThreads, 0, st>>>(3 * n, z, p, sc);
   CK(cudaGetLastError());
-}
-
-// ---------------------------------------------------------------------- grouped (warm start)
-template <int NQ>
-BAL_D void grp_warp_accum(int g, const double (&v)[NQ], double* bucket /*[warps][kMaxGroups][NQ]*/) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned pending = __ballot_sync(0xffffffffu, g >= 0);
-  while (pending) {
-    const int leader = __ffs(pending) - 1;
-    const int gl = __shfl_sync(0xffffffffu, g, leader);
-    const unsigned members = __ballot_sync(0xffffffffu, g == gl);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      double s = (g == gl) ? v[q] : 0.0;
-      s = warp_sum(s);
-      if (lane == leader) bucket[(w * kMaxGroups + gl) * NQ + q] += s;
-    }
-    pending &= ~members;
-  }
-}
-
-// block buckets -> per-block partials [blk][kMaxGroups][NQ]; last block -> totals (thread g)
-template <int NQ>
-BAL_D bool grp_finish(double* bucket, double* partials, unsigned* counter, int G, double (&tot)[NQ]) {
-  __shared__ bool last;
-  constexpr int W = kVecThreads / 32;
-  __syncthreads();
-  for (int t = threadIdx.x; t < G * NQ; t += blockDim.x) {
-    const int g = t / NQ, q = t % NQ;
-    double s = 0.0;
-    for (int w = 0; w < W; ++w) s += bucket[(w * kMaxGroups + g) * NQ + q];
-    partials[((size_t)blockIdx.x * kMaxGroups + g) * NQ + q] = s;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-  if (threadIdx.x < G) {
-    const int g = threadIdx.x;
-    for (int q = 0; q < NQ; ++q) {
-      double s = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) s += partials[((size_t)b * kMaxGroups + g) * NQ + q];
-      tot[q] = s;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *counter = 0u;
-  return true;
-}
-
-BAL_D void ws_zero_bucket(double* bucket, int nq) {
-  for (int t = threadIdx.x; t < (kVecThreads / 32) * kMaxGroups * nq; t += blockDim.x) bucket[t] = 0.0;
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kVecThreads)

@@ -4,12 +4,25 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "common.cuh"
+
 namespace bal {
 
 #ifndef BAL_SPMV_TILE_ROWS
 #define BAL_SPMV_TILE_ROWS 16
 #endif
 constexpr int kSpmvTileRows = BAL_SPMV_TILE_ROWS;  // block rows per SpMV tile
+
+// TMA-staged symmetric SpMV (k_spmv.cu): rows per tile, threads per CTA, bulk-copy ring stages
+#ifndef BAL_SYM_TILE_ROWS
+#define BAL_SYM_TILE_ROWS 64
+#endif
+#ifndef BAL_SYM_STAGES
+#define BAL_SYM_STAGES 2
+#endif
+constexpr int kSymR = BAL_SYM_TILE_ROWS;
+constexpr int kSymThreads = 256;
+constexpr int kSymStages = BAL_SYM_STAGES;
 
 constexpr int kElasticThreads = 128;
 constexpr int kMaxGroups = 64;
@@ -47,6 +60,19 @@ struct Bsr {
   const int* m_col = nullptr;      // [m_row_ptr[n]]
   int nmirror = 0;
   int tile_cap_s = 0;  // staged-full mode: max blocks of a kTileRows-row tile (0 = not staged)
+  // TMA-staged symmetric kernel (k_spmv.cu): the mirror entries of row j split by whether the
+  // stored block's row i lies in j's kSymR-row tile (then the block is in shared memory: mi_loc =
+  // its index within the tile's stored range) or in a later tile (gathered: mo_pos, mo_col = i).
+  const int* mi_row_ptr = nullptr;             // [n+1]
+  const unsigned short* mi_loc = nullptr;      // [mi_row_ptr[n]]
+  const int* mo_row_ptr = nullptr;             // [n+1]
+  const int* mo_pos = nullptr;                 // [mo_row_ptr[n]]
+  const int* mo_col = nullptr;                 // [mo_row_ptr[n]]
+  int tcap = 0, tocap = 0;                     // max stored blocks / out-of-tile mirrors of a tile
+  // rows computed by the SpMV kernels: [r0, r1) (r1 < 0 = n); a rank's owned range in the
+  // partitioned solve, kSymR-aligned so tiles never straddle ranks
+  int r0 = 0, r1 = -1;
+  BAL_HD int row_end() const { return r1 < 0 ? n : r1; }
 };
 // static-part SpMV layout: 0 = symmetric (lower + mirror index), 1 = full BSR streamed by the tiled
 // kernel, 2 = full BSR staged through shared memory with cp.async.  BAL_SPMV=sym|full|staged.
@@ -78,6 +104,11 @@ struct GrpScal {
 };
 
 void spmv_init_grids();
+bool spmv_sym_usable(const Bsr& S);
+void spmv_sym_prepare(const Bsr& S);
+// TMA-staged symmetric SpMV; sc != nullptr fuses p^T A p and alpha (DOT).  false = not usable.
+bool launch_spmv_sym(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,
+                     double* partials, unsigned* counter, PcgScal* sc);
 void spmv_prepare(const Bsr& S);
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y);
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,

@@ -146,6 +146,8 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
 
 int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
               int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats) {
+  if (c->dist.active)
+    return pcg_solve_dist(c, rhs, x0, x_out, warm, tol, window, max_iters, ws_tol, ws_max, stats);
   cudaStream_t st = c->st;
   const int N = c->N;
   const Bsr S = c->static_bsr(), C = c->contact_bsr();
@@ -240,6 +242,10 @@ __global__ void k_set_resume(PcgScal* sc, int extra, int cap) {
 }
 
 void pcg_resume(bal_ctx* c, int extra, double* x_out, bal_pcg_stats* stats) {
+  if (c->dist.active) {
+    pcg_resume_dist(c, extra, x_out, stats);
+    return;
+  }
   cudaStream_t st = c->st;
   k_set_resume<<<1, 1, 0, st>>>(c->scal.ptr, extra, c->prm.max_pcg);
   c->launches += 1;

@@ -250,6 +250,40 @@ def make_single_tet(seed=0, height=0.05, E=1e5, nu=0.4, rho=1e3, speed=0.0, vt=0
     return sb.build([(E, nu, rho)], "tet", chi=chi)
 
 
+def make_incline(seed=0, ratio=0.8, chi=0.3, E=1e5, nu=0.4, rho=1e3, gap=5e-4, size=0.1):
+    """Friction fixture (acceptance 9): one tet resting on a fixed plane inclined at
+    tan(theta) = ratio * chi about the z axis.  The tet's base face is parallel to the incline, `gap`
+    above it, at rest; a small generic yaw about the incline normal and an offset from the plane's
+    diagonal keep the base vertices inside the plane triangles (no type-resolution ties, Q27).
+    Returns the scene; scene["incline_normal"] / ["incline_down"] are the unit normal and the unit
+    downhill direction (geometry only, no method arithmetic)."""
+    rng = np.random.default_rng(seed)
+    theta = np.arctan(ratio * chi)
+    c, s = np.cos(theta), np.sin(theta)
+    down = np.array([c, -s, 0.0])     # downhill along the slope (x decreasing height)
+    nrm = np.array([s, c, 0.0])       # upward unit normal of the incline
+    side = np.array([0.0, 0.0, 1.0])
+    yaw = rng.uniform(0.2, 0.6)
+    cy, sy = np.cos(yaw), np.sin(yaw)
+    base = size * np.array([[-0.5, -0.4], [0.5, -0.3], [0.05, 0.6]])  # (downhill, side) coordinates
+    base = base @ np.array([[cy, sy], [-sy, cy]]).T + np.array([0.31, 0.13])
+    pts = [gap * nrm + b[0] * down + b[1] * side for b in base]
+    apex = gap * nrm + 0.8 * size * nrm + (base.mean(0)[0] * down + base.mean(0)[1] * side)
+    x = np.array(pts + [apex])
+    tets = _orient(x, np.array([[0, 1, 2, 3]]))
+    sb = SceneBuilder()
+    sb.add_body(x, tets, 0)
+    half = 2.0
+    px = np.array([-half * down - half * side, half * down - half * side, half * down + half * side,
+                   -half * down + half * side])
+    sb.add_obstacle(px, np.array([[0, 2, 1], [0, 3, 2]]) if np.dot(np.cross(px[2] - px[0], px[1] - px[0]), nrm) > 0
+                    else np.array([[0, 1, 2], [0, 2, 3]]))
+    sc = sb.build([(E, nu, rho)], f"incline-{ratio:g}chi", chi=chi)
+    sc["incline_normal"] = nrm
+    sc["incline_down"] = down
+    return sc
+
+
 def perturbed(scene, seed, scale):
     """Copy of `scene` with x0 randomly perturbed (free nodes only) by N(0, scale^2)."""
     rng = np.random.default_rng(seed)

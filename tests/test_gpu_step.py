@@ -139,3 +139,51 @@ def test_frame_slices_equal_bal_step():
         x, v = xn, vn
     with pytest.raises(bal.BalError):
         bal.bal_frame_iterate(ctx, 1)  # no frame in progress
+
+
+TRACE_INT = ("nA", "nAp", "rebuilt", "pcg_iters", "pcg_stop", "halvings", "resumes", "safeguard")
+
+
+def _trace_equal(tg, to, rel=1e-6):
+    """Decision trace (SURVEY c.4): identical integer decisions, alpha_CCD / alpha / ||e||/||e0|| and
+    sigma within rel."""
+    assert len(tg) == len(to)
+    for g, o in zip(tg, to):
+        for k in TRACE_INT:
+            assert int(g[k]) == int(o[k]), (k, g, o)
+        for k in ("alpha_ccd", "alpha", "rel_e", "sigma"):
+            assert g[k] == pytest.approx(float(o[k]), rel=rel, abs=1e-300), (k, g[k], o[k])
+
+
+def test_cubes_decision_trace_equality():
+    """C1, 10 steps: the GPU's per-Newton-iteration decision trace equals the oracle's (|A|, |A'|,
+    rebuild flag, PCG iterations and stop reason, halvings, resumes, safeguard; alpha_CCD, alpha,
+    sigma, ||e||/||e0|| to 1e-6)."""
+    sc = scenes.make_cubes(1)
+    _xg, tg, _ = gpu_steps(sc, 10)
+    _xo, to = oracle_steps(sc, 10)
+    for k in range(10):
+        _trace_equal(tg[k], to[k])
+
+
+@pytest.mark.parametrize("ratio", [0.8, 1.2])
+def test_incline_friction_on_gpu(ratio):
+    """SPEC S:587 on the GPU: tan(theta) = 0.8 chi creeps at the closed-form stick velocity
+    eps_v (1 - sqrt(1 - r)); 1.2 chi slides with dv = g h (sin - chi cos) per step; positions match
+    the oracle step by step (1e-6 of the displacement) and the decision traces are equal."""
+    chi = 0.3
+    sc = scenes.make_incline(0, ratio=ratio, chi=chi)
+    n = 6
+    xg, tg, _ = gpu_steps(sc, n)
+    xo, to = oracle_steps(sc, n)
+    for k in range(n):
+        assert _rel(xg[k], xo[k], xo[k] - sc["x0"]) <= 1e-6, k
+        _trace_equal(tg[k], to[k])
+    h = sc["params"]["h"]
+    vd = [float(((xg[k][:4] - (xg[k - 1][:4] if k else sc["x0"][:4])).mean(0) / h) @ sc["incline_down"])
+          for k in range(n)]
+    if ratio < 1:
+        assert vd[-1] == pytest.approx(1e-3 * (1 - np.sqrt(1 - ratio)), rel=2e-3)
+    else:
+        th = np.arctan(ratio * chi)
+        np.testing.assert_allclose(np.diff(vd)[2:], 9.81 * h * (np.sin(th) - chi * np.cos(th)), rel=2e-3)

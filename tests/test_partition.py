@@ -119,3 +119,115 @@ def test_distributed_spmv_and_dot_data_flow_gloo():
     for k in range(world):
         assert out[k][3] == pytest.approx(float(x @ y), rel=1e-12)
         assert out[k][4] > 0  # ranks do exchange values
+
+
+def _aligned_bounds(rp, world, align=64):
+    import paper_2407_00046_b200 as bal
+    N = len(rp) - 1
+    b = bal.bal_partition_rows(np.diff(rp).astype(np.int64), world)
+    for k in range(1, world):
+        b[k] = max(b[k - 1], min((int(b[k]) + align // 2) // align * align, N))
+    return b
+
+
+def test_halo_plan_matches_reference():
+    """bal_halo_plan: the send list of rank k to m is exactly the owned rows of k adjacent to rows
+    of m, the receive list of k from m exactly m's rows adjacent to k's rows, and the send list of
+    k to m equals the receive list of m from k (the exchange is consistent)."""
+    import paper_2407_00046_b200 as bal
+    rp, col, N = _pattern(_scene())
+    world = 4
+    b = _aligned_bounds(rp, world)
+    owner = np.searchsorted(b, np.arange(N), side="right") - 1
+    plans = [bal.bal_halo_plan(rp, col, b, k) for k in range(world)]
+    for k in range(world):
+        sp_, si, rpp, ri = plans[k]
+        for m in range(world):
+            s_km = si[sp_[m]:sp_[m + 1]]
+            r_km = ri[rpp[m]:rpp[m + 1]]
+            if m == k:
+                assert len(s_km) == 0 and len(r_km) == 0
+                continue
+            rows_k = np.arange(b[k], b[k + 1])
+            need = [i for i in rows_k if np.any(owner[col[rp[i]:rp[i + 1]]] == m)]
+            np.testing.assert_array_equal(s_km, need)
+            ghost = np.unique([j for i in rows_k for j in col[rp[i]:rp[i + 1]] if owner[j] == m])
+            np.testing.assert_array_equal(r_km, ghost.astype(np.int32) if len(ghost) else np.zeros(0, np.int32))
+            sp2, si2, _rp2, _ri2 = plans[m]
+            np.testing.assert_array_equal(r_km, si2[sp2[k]:sp2[k + 1]])
+
+
+def test_halo_pack_unpack_roundtrip():
+    import paper_2407_00046_b200 as bal
+    rng = np.random.default_rng(3)
+    v = rng.normal(size=30)
+    idx = np.array([7, 2, 9], np.int32)
+    buf = bal.bal_halo_pack(idx, v)
+    np.testing.assert_array_equal(buf, v.reshape(-1, 3)[idx].ravel())
+    w = np.zeros(30)
+    bal.bal_halo_unpack(idx, buf, w)
+    np.testing.assert_array_equal(w.reshape(-1, 3)[idx], v.reshape(-1, 3)[idx])
+    assert np.count_nonzero(w) == 9
+
+
+def _halo_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2407_00046_b200 as bal
+    rp, col, N = _pattern(_scene())
+    rng = np.random.default_rng(0)
+    vals = rng.normal(size=len(col))
+    A = sp.csr_matrix((vals, col, rp), shape=(N, N))
+    x = rng.normal(size=(N, 3))
+    b = _aligned_bounds(rp, world)
+    r0, r1 = int(b[rank]), int(b[rank + 1])
+    sp_, si, rpp, ri = bal.bal_halo_plan(rp, col, b, rank)
+    xl = np.full((N, 3), np.nan)
+    xl[r0:r1] = x[r0:r1]
+    # the library's halo: pack the owned boundary rows per peer, point-to-point exchange, unpack
+    reqs, bufs = [], {}
+    for m in range(world):
+        if sp_[m + 1] > sp_[m]:
+            sb = torch.as_tensor(bal.bal_halo_pack(si[sp_[m]:sp_[m + 1]], xl))
+            reqs.append(dist.isend(sb, m))
+            bufs[("s", m)] = sb
+        if rpp[m + 1] > rpp[m]:
+            rb = torch.zeros(3 * int(rpp[m + 1] - rpp[m]), dtype=torch.float64)
+            reqs.append(dist.irecv(rb, m))
+            bufs[("r", m)] = rb
+    for q in reqs:
+        q.wait()
+    flat = xl.ravel()
+    for m in range(world):
+        if ("r", m) in bufs:
+            bal.bal_halo_unpack(ri[rpp[m]:rpp[m + 1]], bufs[("r", m)].numpy(), flat)
+    xl = flat.reshape(N, 3)
+    y_own = A[r0:r1] @ xl  # NaN if the plan missed a ghost
+    d = torch.tensor([float(np.sum(x[r0:r1] * y_own))], dtype=torch.float64)
+    dist.all_reduce(d)
+    out[rank] = (r0, r1, y_own, float(d.item()), int(sp_[-1]), int(rpp[-1]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_halo_exchange_spmv_gloo():
+    """World-2 gloo run of the library's own halo plan + pack/unpack (bal_halo_plan, bal_halo_pack,
+    bal_halo_unpack): each rank computes its owned rows of A x from owned + received ghost values
+    only, and the all-reduced dot equals the single-process one."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_halo_worker, args=(world, port, out), nprocs=world, join=True)
+    rp, col, N = _pattern(_scene())
+    rng = np.random.default_rng(0)
+    A = sp.csr_matrix((rng.normal(size=len(col)), col, rp), shape=(N, N))
+    x = rng.normal(size=(N, 3))
+    y = A @ x
+    y_dist = np.concatenate([out[k][2] for k in range(world)])
+    assert np.all(np.isfinite(y_dist))
+    np.testing.assert_allclose(y_dist, y, rtol=1e-13, atol=1e-13)
+    for k in range(world):
+        assert out[k][3] == pytest.approx(float(np.sum(x * y)), rel=1e-12)
+        assert out[k][4] > 0 and out[k][5] > 0
