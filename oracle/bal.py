@@ -321,8 +321,11 @@ class Oracle:
                 alpha = min(1.0, a_ccd)
                 L0, _n0, S0 = self.energy(x, st, cpt, cee)
                 halvings = 0
+                ls_margin = np.inf  # closest accept/reject decision to its threshold, relative to S
                 while alpha >= float(p["alpha_min"]):
                     L1, n1, S1 = self.energy(x + alpha * P, st, cpt, cee)
+                    if np.isfinite(L1):
+                        ls_margin = min(ls_margin, abs(L1 - L0 - LS_ROUND * max(S0, S1)) / max(S0, S1))
                     # R-LS1: accept when L does not increase beyond its FP64 evaluation error; an
                     # infeasible trial (J <= 0, d <= 0, NaN) has L = +inf and is never accepted
                     if (n1 <= int(p["max_constraints"]) and np.isfinite(L1)
@@ -348,7 +351,8 @@ class Oracle:
                                   sigma=st["sigma"], groups=dict(zip(gvals.tolist(), gcnt.tolist())),
                                   ws_iters=ws_it, pcg_iters=pst.k, pcg_stop=pst.stop, alpha_ccd=a_ccd,
                                   alpha=alpha, halvings=halvings, resumes=resumes, safeguard=safeguard,
-                                  rel_e=en / e0))
+                                  rel_e=en / e0, nA_margin=cm.activation_margin(x, pt, ee, dhat),
+                                  ls_margin=ls_margin, pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
             if en <= float(p["newton_rel_tol"]) * e0:
                 x = x_new
                 converged = True

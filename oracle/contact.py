@@ -255,6 +255,17 @@ def constraint_set(x, pt, ee, dhat):
     return keys[m], d[m]
 
 
+def activation_margin(x, pt, ee, dhat):
+    """min over the candidate feature pairs of |d - dhat| / dhat: how close the d < dhat membership
+    decision of the active set came to a tie (decision-trace tooling, SURVEY c.4)."""
+    m = np.inf
+    for ftype, pairs in ((PT, pt), (EE, ee)):
+        if len(pairs):
+            D, _t, _l = resolve_features(x, ftype, pairs)
+            m = min(m, float(np.min(np.abs(np.sqrt(D) - dhat))) / dhat)
+    return m
+
+
 def key_distance(x, keys):
     """True feature distance d_i(x) of each key (re-resolving its sub-type at x)."""
     d = np.zeros(len(keys))

@@ -15,6 +15,10 @@ TEST INFRASTRUCTURE (see oracle/__init__.py).
        oscillates by orders of magnitude on the stiff C4 systems, so a residual-minimum test stops
        CG before it ever improves on x0 -- measured, profiles/pcg_stagnation_r01.md.)
      iteration cap; NaN.
+ - pcg_cg: the same block-Jacobi PCG in Chronopoulos-Gear form (one inner-product phase per
+   iteration: (r,u) and (Au,u) together), the parity partner of the GPU's single-reduction PCG
+   (SURVEY §8(c) c.1 step 7).  Equal to the textbook iterates in exact arithmetic (pinned in
+   tests/test_oracle_solver.py); same stop rules.
  - warm start: for each stiffness group G an
    independent block-Jacobi PCG on A_GG (cross-group blocks skipped), zero initial guess,
    stop at ||r_G|| <= ws_tol ||b_G|| or ws_max iterations; the union is the initial guess x_0.
@@ -87,9 +91,83 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
         st.k += 1
 
 
+def stop_margin(st, tol):
+    """How close the convergence test ||r_k|| <= tol ||b|| came to a tie at the last two iterates
+    (relative): decision-trace tooling (SURVEY c.4); another PCG form may stop one iteration apart
+    when this is at rounding level."""
+    ref = tol * st.bnorm
+    if ref <= 0.0:
+        return np.inf
+    return min(abs(h / ref - 1.0) for h in st.hist[-2:])
+
+
 def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000):
     st = pcg_start(A, b, x0, Dinv)
     return pcg_run(A, Dinv, st, tol, window, max_iters)
+
+
+class CGState(PCGState):
+    """Chronopoulos-Gear state (x, r, u, p, s, w and the scalars) for App. B resumes."""
+
+
+def cg_start(A, b, x0, Dinv):
+    """Chronopoulos-Gear PCG (Chronopoulos & Gear 1989, preconditioned form), M = blockdiag(D_j):
+        r_0 = b - A x_0, u_0 = M^-1 r_0, w_0 = A u_0, gam_0 = (r_0,u_0), delta_0 = (w_0,u_0),
+        alpha_0 = gam_0/delta_0, beta_0 = 0, p_-1 = s_-1 = 0;
+        p_k = u_k + beta_k p_{k-1};  s_k = w_k + beta_k s_{k-1}   (s_k = A p_k)
+        x_{k+1} = x_k + alpha_k p_k;  r_{k+1} = r_k - alpha_k s_k;  u_{k+1} = M^-1 r_{k+1};  w_{k+1} = A u_{k+1}
+        gam_{k+1} = (r_{k+1},u_{k+1}); delta_{k+1} = (w_{k+1},u_{k+1});  beta_{k+1} = gam_{k+1}/gam_k
+        alpha_{k+1} = gam_{k+1} / (delta_{k+1} - beta_{k+1} gam_{k+1} / alpha_k)."""
+    x = x0.copy()
+    r = b - A @ x
+    u = apply_block(Dinv, r)
+    st = CGState(x, r, u, np.zeros_like(b), float(r @ u), [float(np.linalg.norm(r))], float(np.linalg.norm(b)))
+    st.u, st.w, st.s = u, A @ u, np.zeros_like(b)
+    delta = float(st.w @ u)
+    st.alpha = st.rz / delta if delta != 0.0 else 0.0
+    st.beta = 0.0
+    return st
+
+
+def cg_run(A, Dinv, st, tol, window, max_iters):
+    """Chronopoulos-Gear iterations on st until a stop condition or st.k reaches max_iters.  Stop
+    rules and their order as pcg_run (App. B, Q14, R-PCG1), checked on ||r_k|| before step k."""
+    while True:
+        rn = st.hist[-1]
+        k = st.k
+        if not np.isfinite(rn):
+            st.stop = STOP_NAN
+            return st
+        if rn <= tol * st.bnorm:
+            st.stop = STOP_CONVERGED
+            return st
+        if k >= window and (st.dec[k] - st.dec[k - window]) <= STALL_REL * st.dec[k]:
+            st.stop = STOP_STAGNATED
+            return st
+        if k >= max_iters:
+            st.stop = STOP_CAP
+            return st
+        st.p = st.u + st.beta * st.p
+        st.s = st.w + st.beta * st.s
+        st.x = st.x + st.alpha * st.p
+        st.r = st.r - st.alpha * st.s
+        st.u = apply_block(Dinv, st.r)
+        st.w = A @ st.u
+        gam_new = float(st.r @ st.u)
+        delta = float(st.w @ st.u)
+        st.dec.append(st.dec[-1] + 0.5 * st.alpha * st.rz)  # phi decrease of step k: alpha_k gam_k / 2
+        beta = gam_new / st.rz if st.rz != 0.0 else 0.0
+        den = delta - beta * gam_new / st.alpha if st.alpha != 0.0 else delta
+        st.alpha = gam_new / den if den != 0.0 else 0.0  # r = 0 exactly: converged, next check stops
+        st.beta = beta
+        st.rz = gam_new
+        st.hist.append(float(np.linalg.norm(st.r)))
+        st.k += 1
+        st.z = st.u
+
+
+def pcg_cg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000):
+    return cg_run(A, Dinv, cg_start(A, b, x0, Dinv), tol, window, max_iters)
 
 
 def warm_start(A, b, groups, Dinv, fixed, tol=1e-2, max_iters=100):

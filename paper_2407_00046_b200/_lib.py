@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbal.so")
+LIB_PATH = os.environ.get("BAL_LIB_PATH") or os.path.join(HERE, "libbal.so")  # override: build variants
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libbal.so not built at {LIB_PATH}: run `python -m paper_2407_00046_b200.build` "

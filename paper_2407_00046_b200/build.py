@@ -13,8 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libbal.so")
+OBJ = os.environ.get("BAL_BUILD_DIR") or os.path.join(HERE, "build")
+LIB = os.environ.get("BAL_LIB_OUT") or os.path.join(HERE, "libbal.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

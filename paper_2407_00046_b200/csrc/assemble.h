@@ -33,7 +33,8 @@ struct DevBuf {
   }
   void upload(const T* h, size_t n, cudaStream_t st) {
     reserve(n);
-    if (n) CK(cudaMemcpyAsync(ptr, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    // h may be an empty vector's data() (nullptr) with n = 1 (minimum-size buffers): reserve only
+    if (n && h) CK(cudaMemcpyAsync(ptr, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
   }
 };
 

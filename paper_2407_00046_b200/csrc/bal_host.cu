@@ -7,54 +7,72 @@
 #include <numeric>
 
 #include "ctx.h"
+#include "reduce.cuh"
 
 using namespace bal;
 
-void SymTilesDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& urow,
-                        const std::vector<int>& upos, const std::vector<int>& ucol, cudaStream_t st) {
-  std::vector<int> mirp(N + 1, 0), morp(N + 1, 0), mopos, mocol;
-  std::vector<unsigned short> miloc;
-  cap = 0;
-  ocap = 0;
-  for (int r0 = 0; r0 < N; r0 += kSymR) {
-    const int r1 = std::min(N, r0 + kSymR);
-    const int s0 = lrow[r0];
-    cap = std::max(cap, lrow[r1] - s0);
-    for (int j = r0; j < r1; ++j) {
-      for (int e = urow[j]; e < urow[j + 1]; ++e) {
-        if (ucol[e] < r1) {
-          miloc.push_back((unsigned short)(upos[e] - s0));
-        } else {
-          mopos.push_back(upos[e]);
-          mocol.push_back(ucol[e]);
-        }
-      }
-      mirp[j + 1] = (int)miloc.size();
-      morp[j + 1] = (int)mopos.size();
+void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, cudaStream_t st) {
+  ready = false;
+  if (getenv("BAL_SPMV_GENERIC") != nullptr || N <= 0) return;
+  int dev = 0, smem_max = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int env = getenv("BAL_TS_BUDGET") ? atoi(getenv("BAL_TS_BUDGET")) : 0;
+  // largest block budget per tile whose kTsStages-stage ring fits the opt-in shared memory
+  TsHost H;
+  bool ok = false;
+  // (kTsMinBlocks CTAs of it per SM; the driver reserves 1 KB of shared memory per CTA)
+  int smem_sm = 0;
+  CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  const size_t per_cta = std::min<size_t>((size_t)smem_max, (size_t)smem_sm / kTsMinBlocks) - 1024;
+  for (int budget : {env > 0 ? env : 768, 704, 640, 576, 512, 448, 384, 320, 288, 256, 224, 192, 160, 128, 96, 64}) {
+    if (!ts_build(N, lrow, lcol, budget, H)) return;
+    if (H.smem <= per_cta) {
+      ok = true;
+      break;
     }
-    ocap = std::max(ocap, morp[r1] - morp[r0]);
   }
-  if (cap >= 65536) {  // local indices are 16-bit: fall back to the generic kernel
-    ready = false;
-    return;
+  if (!ok) return;
+  std::vector<int4> hd(H.ntiles + 1);
+  for (int t = 0; t <= H.ntiles; ++t) {
+    if (H.meta_off[t] / 16 >= (1ll << 31)) return;
+    hd[t] = make_int4((int)(H.meta_off[t] / 16), H.tile_s0[t], H.tile_r0[t], 0);
   }
-  mi_rp.upload(mirp.data(), mirp.size(), st);
-  mo_rp.upload(morp.data(), morp.size(), st);
-  mi_loc.upload(miloc.data(), std::max<size_t>(miloc.size(), 1), st);
-  mo_pos.upload(mopos.data(), std::max<size_t>(mopos.size(), 1), st);
-  mo_col.upload(mocol.data(), std::max<size_t>(mocol.size(), 1), st);
-  ready = true;
-}
-
-void SymTilesDev::wire(Bsr& b) const {
-  if (!ready) return;
-  b.mi_row_ptr = mi_rp.ptr;
-  b.mi_loc = mi_loc.ptr;
-  b.mo_row_ptr = mo_rp.ptr;
-  b.mo_pos = mo_pos.ptr;
-  b.mo_col = mo_col.ptr;
-  b.tcap = cap;
-  b.tocap = ocap;
+  desc.upload(hd.data(), hd.size(), st);
+  pin_ptr.upload(H.pin_ptr.data(), H.pin_ptr.size(), st);
+  meta.upload(H.meta.data(), std::max<size_t>(H.meta.size(), 16), st);
+  part.reserve(3 * (size_t)std::max(H.nslots, 1));
+  plan = TsPlan();
+  plan.n = N;
+  plan.ntiles = H.ntiles;
+  plan.nslots = H.nslots;
+  plan.desc = desc.ptr;
+  plan.cap_rows = H.cap_rows;
+  plan.o_crp = H.o_crp;
+  plan.meta = meta.ptr;
+  plan.pin_ptr = pin_ptr.ptr;
+  plan.part = part.ptr;
+  plan.o_meta = H.o_meta;
+  plan.o_val = H.o_val;
+  plan.o_vt = H.o_vt;
+  plan.o_xv = H.o_xv;
+  plan.stage_bytes = H.stage_bytes;
+  plan.o_scratch = H.o_scratch;
+  plan.cap_nb = H.cap_nb;
+  plan.cap_cs = H.cap_cs;
+  plan.cap_tp = H.cap_tp;
+  plan.smem = H.smem;
+  plan.meta_bytes = (long long)H.meta.size();
+  plan.ncross_total = H.ncross_total;
+  CK(cudaStreamSynchronize(st));
+  const int grid = ts_prepare(plan);
+  ready = grid > 0;
+  if (getenv("BAL_VERBOSE"))
+    fprintf(stderr,
+            "[bal-ts] N=%d tiles=%d grid=%d cap_nb=%d cap_rows=%d cap_x=%d cap_meta=%d smem=%zu slots=%d "
+            "cross=%lld meta=%lld B\n",
+            N, H.ntiles, grid, H.cap_nb, H.cap_rows, H.cap_x, H.cap_meta, H.smem, H.nslots, H.ncross_total,
+            (long long)H.meta.size());
 }
 
 bal::Bsr bal_ctx::static_bsr() const {
@@ -69,7 +87,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.m_pos = lb_upos.ptr;
     b.m_col = lb_ucol.ptr;
     b.nmirror = lb_nu;
-    lb_tiles.wire(b);
+    lb_ts.wire(b);
   } else if (sp_sym) {
     b.nnzb = sp.nl;
     b.row_ptr = sp.l_row_ptr;
@@ -79,7 +97,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.m_pos = sp.u_pos;
     b.m_col = sp.u_col;
     b.nmirror = sp.nu;
-    sp_tiles.wire(b);
+    sp_ts.wire(b);
   } else {
     b.nnzb = sp.nnzb;
     b.row_ptr = sp.row_ptr;
@@ -410,14 +428,13 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     c->sp_sym = spmv_symmetric_enabled();
     if (c->sp_sym) {
       c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1) + 2);  // + 16 B slack for the bulk copies
-      if (getenv("BAL_SPMV_GENERIC") == nullptr) c->sp_tiles.build(N, lrow, urow, upos, ucol, st);
+      c->sp_ts.build(N, lrow, lcol, st);
     }
     for (int r0 = 0; r0 < N; r0 += kSpmvTileRows)
       c->sp.tile_cap_full = std::max(c->sp.tile_cap_full,
                                      row_ptr[std::min(N, r0 + kSpmvTileRows)] - row_ptr[r0]);
     spmv_init_grids();
     spmv_prepare(c->static_bsr());
-    spmv_sym_prepare(c->static_bsr());
   }
   c->sval.reserve(9 * (size_t)nnzb);
   c->stage_e.reserve(90 * (size_t)std::max(T, 1));
@@ -430,7 +447,9 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->grp_c.reserve(N);
   c->y.reserve(3 * (size_t)N);
   c->xt.reserve(3 * (size_t)N);
-  for (auto* b : {&c->pr, &c->pz, &c->pp, &c->pq, &c->px, &c->tmp_a, &c->tmp_b}) b->reserve(3 * (size_t)N);
+  for (auto* b : {&c->pr, &c->pz, &c->pp, &c->pq, &c->px, &c->ps, &c->tmp_a, &c->tmp_b}) b->reserve(3 * (size_t)N);
+  c->upart.reserve(2 * (size_t)kVecBlocks);
+  c->dpart.reserve(4 * (size_t)kSMs);
   c->partials.reserve((size_t)kRedBlocks * kMaxGroups * 4 + 16 * kSMs * 4);
   c->red.reserve(kRedBlocks + 16);  // [0, kRedBlocks) partials, then scalar outputs
   c->counter.reserve(1);
@@ -594,7 +613,7 @@ bal_status bal_spmv(bal_ctx* c, const double* v, double* y) {
   if (!c || !v || !y) return BAL_E_INVALID_ARG;
   return guard(c, [&]() {
     launch_spmv(c->st, c->static_bsr(), c->contact_bsr(), v, y);
-    c->launches += 1;
+    c->launches += ts_usable(c->static_bsr()) ? 2 : 1;
     CK(cudaStreamSynchronize(c->st));
     return BAL_OK;
   });
@@ -602,11 +621,12 @@ bal_status bal_spmv(bal_ctx* c, const double* v, double* y) {
 
 bal_status bal_spmv_rows(bal_ctx* c, int32_t r0, int32_t r1, const double* v, double* y) {
   if (!c || !v || !y || r0 < 0 || r1 < r0 || r1 > c->N) return BAL_E_INVALID_ARG;
-  if (r0 % kSymR != 0 || (r1 != c->N && r1 % kSymR != 0)) return BAL_E_INVALID_ARG;
+  if (r0 % kPartAlign != 0 || (r1 != c->N && r1 % kPartAlign != 0)) return BAL_E_INVALID_ARG;
   return guard(c, [&]() {
     Bsr S = c->static_bsr();
     S.r0 = r0;
     S.r1 = r1;
+    S.ts = nullptr;  // the partitioned path's row-range kernel (pcg_dist.cu)
     if (r1 > r0) launch_spmv(c->st, S, c->contact_bsr(), v, y);
     c->launches += 1;
     CK(cudaStreamSynchronize(c->st));
@@ -680,8 +700,7 @@ bal_status bal_load_bsr(bal_ctx* c, const bal_bsr_host* b) {
       c->lb_upos.upload(upos.data(), std::max<size_t>(upos.size(), 1), st);
       c->lb_ucol.upload(ucol.data(), std::max<size_t>(ucol.size(), 1), st);
       lcol.resize(lcol.size() - 8);
-      if (getenv("BAL_SPMV_GENERIC") == nullptr) c->lb_tiles.build(N, lrow, urow, upos, ucol, st);
-      spmv_sym_prepare(c->static_bsr());
+      c->lb_ts.build(N, lrow, lcol, st);
     }
 
     // diagonal inverse from the loaded blocks (host: test path only)

@@ -9,16 +9,19 @@
 #include "keys.h"
 #include "halo.h"
 
-// Device copy of the TMA-staged symmetric SpMV's per-row mirror split (k_spmv.cu, Bsr::mi_*/mo_*).
-struct SymTilesDev {
-  bal::DevBuf<int> mi_rp, mo_rp, mo_pos, mo_col;
-  bal::DevBuf<unsigned short> mi_loc;
-  int cap = 0, ocap = 0;
+// Device copy of a tile-symmetric SpMV plan (k_spmv_ts.cu) + its partial-slot work buffer.
+struct TsDev {
+  bal::DevBuf<int> pin_ptr;
+  bal::DevBuf<int4> desc;
+  bal::DevBuf<unsigned char> meta;
+  bal::DevBuf<double> part;
+  bal::TsPlan plan;
   bool ready = false;
-  // lower CSR (row_ptr lrow[N+1]) + mirror index (urow[N+1], upos/ucol: lower position of (j, i), j)
-  void build(int N, const std::vector<int>& lrow, const std::vector<int>& urow, const std::vector<int>& upos,
-             const std::vector<int>& ucol, cudaStream_t st);
-  void wire(bal::Bsr& b) const;
+  // lower CSR (lrow[N+1], lcol) -> plan on the device; ready = false when the kernel cannot be used
+  void build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, cudaStream_t st);
+  void wire(bal::Bsr& b) const {
+    if (ready) b.ts = &plan;
+  }
 };
 
 // Partitioned solve state (pcg_dist.cu).  active = the distributed PCG path is used.
@@ -68,7 +71,7 @@ struct bal_ctx {
   bal::DevBuf<int> sp_lpos, sp_lrow, sp_lcol, sp_urow, sp_upos, sp_ucol;  // symmetric SpMV copy
   bal::DevBuf<double> lval;
   bool sp_sym = false;
-  SymTilesDev sp_tiles;
+  TsDev sp_ts;
   // ---- elastic stencils
   bal::DevBuf<double> stage_e, grad_e, lbar_e;
   // ---- contact + friction stencils (friction appended after contact)
@@ -87,13 +90,14 @@ struct bal_ctx {
   bal::DevBuf<int> lb_row_ptr, lb_col;
   bal::DevBuf<double> lb_val;
   int lb_nnzb = 0;
-  // symmetric copy of the loaded system (lower + diagonal blocks, mirror index, tiles)
+  // symmetric copy of the loaded system (lower + diagonal blocks, mirror index, SpMV plan)
   bal::DevBuf<int> lb_lrow, lb_lcol, lb_urow, lb_upos, lb_ucol;
   bal::DevBuf<double> lb_lval;
   int lb_nl = 0, lb_nu = 0;
-  SymTilesDev lb_tiles;
+  TsDev lb_ts;
   // ---- PCG
-  bal::DevBuf<double> pr, pz, pp, pq, px, partials, hist;
+  bal::DevBuf<double> pr, pz, pp, pq, px, ps, partials, hist;
+  bal::DevBuf<double> upart, dpart;  // single-reduction PCG: update-kernel and SpMV block partials
   bal::DevBuf<unsigned> counter;
   bal::DevBuf<bal::PcgScal> scal;
   bal::DevBuf<bal::GrpScal> gscal;
@@ -115,13 +119,18 @@ struct bal_ctx {
     const double Cb = loaded_bsr ? 0.0 : 0.5 * (cw.nslots - cw.nrows);
     return 72.0 * n + 76.0 * E + 4.0 * (n + 1) + 80.0 * Cb + 48.0 * n;
   }
-  // bytes the SpMV kernel as configured must move at minimum: symmetric mode streams lower +
-  // diagonal blocks (76 B with the column) and reads column + mirror index (8 B) per upper slot;
-  // full mode streams every stored block
+  // bytes the SpMV kernel as configured must move at minimum: the tile-symmetric kernel streams
+  // lower + diagonal values (72 B), the tile metadata, v rows, out-of-tile v, y rows and partials;
+  // the generic symmetric kernel streams lower + diagonal blocks (76 B with the column) and reads
+  // column + mirror index (8 B) per upper slot; full mode streams every stored block
   double spmv_moved_bytes() const {
     const double n = N;
     const double cc = loaded_bsr ? 0 : cw.nslots;
     const double contact = cc > 0 ? 76.0 * cc + 4.0 * (n + 1) : 0.0;
+    const TsDev& ts = loaded_bsr ? lb_ts : sp_ts;
+    if (ts.ready)
+      return 72.0 * (loaded_bsr ? lb_nl : sp.nl) + (double)ts.plan.meta_bytes + 48.0 * n +
+             24.0 * (double)ts.plan.ncross_total + 24.0 * ts.plan.nslots + contact;
     if (loaded_bsr) return 76.0 * lb_nnzb + 4.0 * (n + 1) + 48.0 * n;
     const double stat = sp_sym ? 76.0 * sp.nl + 8.0 * sp.nu + 8.0 * (n + 1) : 76.0 * sp.nnzb + 4.0 * (n + 1);
     return stat + contact + 48.0 * n;

@@ -395,7 +395,10 @@ void spmv_init_grids() {  // occupancy queries outside any stream capture (calle
 
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y) {
   if (S.n <= 0) return;
-  if (launch_spmv_sym(st, S, C, v, y, nullptr, nullptr, nullptr)) return;
+  if (ts_usable(S)) {
+    launch_spmv_ts(st, S, C, v, y, S.ts->part, true);
+    return;
+  }
   if (spmv_sf_usable(S)) {
     size_t sm = 0;
     const int g = spmv_sf_grid<false>(S, sm);
@@ -412,7 +415,6 @@ void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, d
 
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* partials,
                      unsigned* counter, PcgScal* sc) {
-  if (launch_spmv_sym(st, S, C, v, y, partials, counter, sc)) return;
   if (spmv_sf_usable(S)) {
     size_t sm = 0;
     const int g = spmv_sf_grid<true>(S, sm);
@@ -633,6 +635,121 @@ void launch_pcg_update_fused(cudaStream_t st, int grid, int n, const double* din
 
 void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, const PcgScal* sc) {
   k_pcg_pupdate<<<kVecBlocks, kVecThreads, 0, st>>>(3 * n, z, p, sc);
+  CK(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------------------------
+// Chronopoulos-Gear block-Jacobi PCG (one grid-wide reduction per iteration; same iterates as the
+// textbook recurrences in exact arithmetic, oracle.linalg.pcg_cg is its parity partner):
+//   init:  r_0 = b - A x_0, u_0 = M^-1 r_0, p_-1 = s_-1 = 0;
+//   SpMV k (k_spmv_ts DOT): w_k = A u_k, and its last CTA reduces (r_k,u_k), (r_k,r_k), (w_k,u_k),
+//          runs the App. B stop test on ||r_k|| and sets beta_k, alpha_k (cg_scalars);
+//   update k (this kernel): p_k = u_k + beta_k p_{k-1}, s_k = w_k + beta_k s_{k-1} (= A p_k),
+//          x += alpha_k p_k, r -= alpha_k s_k, u = M^-1 r, block partials of (r,u), (r,r) for the
+//          next SpMV's reduction.  w_k = the SpMV's owned rows + the cross-tile partials of row i.
+__global__ void __launch_bounds__(kVecThreads)
+k_cg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, const double* __restrict__ dinv,
+          double* __restrict__ r, double* __restrict__ u, double* __restrict__ p, double* __restrict__ s,
+          double* __restrict__ upart, double* partials, unsigned* counter, PcgScal* sc, double* hist) {
+  double g = 0.0, rr = 0.0, bb = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const size_t j = 3 * (size_t)i + c;
+      const double bj = b[j];
+      rv[c] = bj - Ax0[j];
+      r[j] = rv[c];
+      p[j] = 0.0;
+      s[j] = 0.0;
+      bb += bj * bj;
+    }
+    double u0, u1, u2;
+    dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
+    u[3 * (size_t)i] = u0;
+    u[3 * (size_t)i + 1] = u1;
+    u[3 * (size_t)i + 2] = u2;
+    g += rv[0] * u0 + rv[1] * u1 + rv[2] * u2;
+    rr += rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2];
+  }
+  __shared__ double sh[kVecThreads / 32];
+  const double bg = block_sum<kVecThreads>(g, sh);
+  const double br = block_sum<kVecThreads>(rr, sh);
+  if (threadIdx.x == 0) {
+    upart[2 * blockIdx.x] = bg;
+    upart[2 * blockIdx.x + 1] = br;
+  }
+  const double loc[1] = {bb};
+  double tot[1];
+  if (last_block_reduce<1, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
+    sc->bnorm = sqrt(tot[0]);
+    sc->k = 0;
+    sc->stop = -1;
+    sc->done = 0;
+    sc->dec = 0.0;
+    sc->rz = sc->alpha = sc->beta = 0.0;
+  }
+}
+
+void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
+                    double* u, double* p, double* s, double* upart, double* partials, unsigned* counter,
+                    PcgScal* sc, double* hist) {
+  k_cg_init<<<kVecBlocks, kVecThreads, 0, st>>>(n, b, Ax0, dinv, r, u, p, s, upart, partials, counter, sc, hist);
+  CK(cudaGetLastError());
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_ptr, const double* __restrict__ part,
+            const double* __restrict__ w, double* __restrict__ u, double* __restrict__ p, double* __restrict__ s,
+            double* __restrict__ x, double* __restrict__ r, double* __restrict__ upart, PcgScal* sc) {
+  if (sc->done) return;
+  const double alpha = sc->alpha, beta = sc->beta;
+  double g = 0.0, rr = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double wi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) wi[c] = w[3 * (size_t)i + c];
+    if (pin_ptr) {
+      const int e0 = pin_ptr[i], e1 = pin_ptr[i + 1];
+      for (int e = e0; e < e1; ++e) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) wi[c] += part[3 * (size_t)e + c];
+      }
+    }
+    double rv[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const size_t j = 3 * (size_t)i + c;
+      const double pj = u[j] + beta * p[j];
+      const double sj = wi[c] + beta * s[j];
+      p[j] = pj;
+      s[j] = sj;
+      x[j] = x[j] + alpha * pj;
+      rv[c] = r[j] - alpha * sj;
+      r[j] = rv[c];
+    }
+    double u0, u1, u2;
+    dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
+    u[3 * (size_t)i] = u0;
+    u[3 * (size_t)i + 1] = u1;
+    u[3 * (size_t)i + 2] = u2;
+    g += rv[0] * u0 + rv[1] * u1 + rv[2] * u2;
+    rr += rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2];
+  }
+  __shared__ double sh[kVecThreads / 32];
+  const double bg = block_sum<kVecThreads>(g, sh);
+  const double br = block_sum<kVecThreads>(rr, sh);
+  if (threadIdx.x == 0) {
+    upart[2 * blockIdx.x] = bg;
+    upart[2 * blockIdx.x + 1] = br;
+    if (blockIdx.x == 0) sc->k = sc->k + 1;  // read by the next SpMV's last CTA only
+  }
+}
+
+void launch_cg_update(cudaStream_t st, int n, const double* dinv, const int* pin_ptr, const double* part,
+                      const double* w, double* u, double* p, double* s, double* x, double* r, double* upart,
+                      PcgScal* sc) {
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, st>>>(n, dinv, pin_ptr, part, w, u, p, s, x, r, upart, sc);
   CK(cudaGetLastError());
 }
 

@@ -4,6 +4,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace bal {
@@ -13,16 +15,28 @@ namespace bal {
 #endif
 constexpr int kSpmvTileRows = BAL_SPMV_TILE_ROWS;  // block rows per SpMV tile
 
-// TMA-staged symmetric SpMV (k_spmv.cu): rows per tile, threads per CTA, bulk-copy ring stages
-#ifndef BAL_SYM_TILE_ROWS
-#define BAL_SYM_TILE_ROWS 64
+// partitioned solve (pcg_dist.cu): rank row ranges are multiples of this (generic SpMV tiles)
+constexpr int kPartAlign = 64;
+
+// tile-symmetric SpMV (k_spmv_ts.cu): threads per CTA, TMA ring stages, max rows per tile
+#ifndef BAL_TS_CONSUMERS
+#define BAL_TS_CONSUMERS 256
 #endif
-#ifndef BAL_SYM_STAGES
-#define BAL_SYM_STAGES 2
+#ifndef BAL_TS_MINB
+#define BAL_TS_MINB 2
 #endif
-constexpr int kSymR = BAL_SYM_TILE_ROWS;
-constexpr int kSymThreads = 256;
-constexpr int kSymStages = BAL_SYM_STAGES;
+#ifndef BAL_TS_STAGES
+#define BAL_TS_STAGES 2
+#endif
+constexpr int kTsConsumers = BAL_TS_CONSUMERS;  // consumer threads (phase 1 / phase 2)
+constexpr int kTsThreads = kTsConsumers + 32;      // + one producer warp
+constexpr int kTsMinBlocks = BAL_TS_MINB;  // resident CTAs per SM the tile budget is sized for
+constexpr int kTsStages = BAL_TS_STAGES;
+#ifndef BAL_TS_SCRATCH_BUFS
+#define BAL_TS_SCRATCH_BUFS 1
+#endif
+constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;  // 2: consecutive tiles' scratch double-buffered
+constexpr int kTsMaxRows = kTsConsumers;  // one consumer thread per owned row
 
 constexpr int kElasticThreads = 128;
 constexpr int kMaxGroups = 64;
@@ -44,6 +58,8 @@ void launch_friction_energy(cudaStream_t st, int n, const double* x, const doubl
                             double* out);
 
 // ---- sparse system (k_linalg.cu)
+struct TsPlan;
+struct PcgScal;
 struct Bsr {
   int n = 0;             // block rows
   int nnzb = 0;          // stored blocks
@@ -60,20 +76,53 @@ struct Bsr {
   const int* m_col = nullptr;      // [m_row_ptr[n]]
   int nmirror = 0;
   int tile_cap_s = 0;  // staged-full mode: max blocks of a kTileRows-row tile (0 = not staged)
-  // TMA-staged symmetric kernel (k_spmv.cu): the mirror entries of row j split by whether the
-  // stored block's row i lies in j's kSymR-row tile (then the block is in shared memory: mi_loc =
-  // its index within the tile's stored range) or in a later tile (gathered: mo_pos, mo_col = i).
-  const int* mi_row_ptr = nullptr;             // [n+1]
-  const unsigned short* mi_loc = nullptr;      // [mi_row_ptr[n]]
-  const int* mo_row_ptr = nullptr;             // [n+1]
-  const int* mo_pos = nullptr;                 // [mo_row_ptr[n]]
-  const int* mo_col = nullptr;                 // [mo_row_ptr[n]]
-  int tcap = 0, tocap = 0;                     // max stored blocks / out-of-tile mirrors of a tile
+  // tile-symmetric plan of the stored part (k_spmv_ts.cu; host-side handle, device arrays)
+  const TsPlan* ts = nullptr;
   // rows computed by the SpMV kernels: [r0, r1) (r1 < 0 = n); a rank's owned range in the
-  // partitioned solve, kSymR-aligned so tiles never straddle ranks
+  // partitioned solve, kPartAlign-aligned so tiles never straddle ranks
   int r0 = 0, r1 = -1;
   BAL_HD int row_end() const { return r1 < 0 ? n : r1; }
 };
+// Tile-symmetric SpMV plan (k_spmv_ts.cu): tiles of consecutive rows, per-tile metadata streamed
+// with the values, partial slots of out-of-tile mirror products sorted by target row.
+struct TsPlan {
+  int n = 0, ntiles = 0, nslots = 0;
+  // [ntiles+1] per tile: metadata offset (16 B units), first stored (lower) block, first row
+  const int4* desc = nullptr;
+  const unsigned char* meta = nullptr;
+  const int* pin_ptr = nullptr;        // [n+1] partial slots targeting row j: [pin_ptr[j], pin_ptr[j+1])
+  double* part = nullptr;              // [3 nslots] work buffer of the partials (owned by the ctx)
+  int cap_nb = 0, cap_rows = 0, cap_cs = 0, cap_tp = 0;
+  size_t o_crp = 0;  // contact row pointers of the tile (cp.async with the out-of-tile v)
+  size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
+  long long meta_bytes = 0, ncross_total = 0;
+};
+struct TsHost {  // host build of a TsPlan (ts_build)
+  std::vector<int> tile_r0, tile_s0, pin_ptr;
+  std::vector<long long> meta_off;
+  std::vector<unsigned char> meta;
+  int ntiles = 0, nslots = 0, cap_nb = 0, cap_rows = 0, cap_x = 0, cap_meta = 0, cap_cs = 0, cap_tp = 0;
+  long long ncross_total = 0;
+  size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, o_crp = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
+};
+// lower CSR (lrow[N+1], lcol: lower + diagonal blocks, ascending column) -> plan; false = unusable
+bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, TsHost& P);
+int ts_prepare(const TsPlan& P);  // grid (0 = does not fit); call outside stream capture
+bool ts_usable(const Bsr& S);
+// y = A v: owned rows to y, cross-tile partials to part; combine = add the partials into y
+void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* part,
+                    bool combine);
+// w_own = A u (+ partials) with the fused single-reduction PCG epilogue (cg_scalars)
+void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* u, double* w, double* part,
+                        double* dpart, unsigned* counter, PcgScal* sc, const double* upart, double* hist);
+// Chronopoulos-Gear PCG (k_linalg.cu): init from A x0 (complete) and the per-iteration update
+void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
+                    double* u, double* p, double* s, double* upart, double* partials, unsigned* counter,
+                    PcgScal* sc, double* hist);
+void launch_cg_update(cudaStream_t st, int n, const double* dinv, const int* pin_ptr, const double* part,
+                      const double* w, double* u, double* p, double* s, double* x, double* r, double* upart,
+                      PcgScal* sc);
+
 // static-part SpMV layout: 0 = symmetric (lower + mirror index), 1 = full BSR streamed by the tiled
 // kernel, 2 = full BSR staged through shared memory with cp.async.  BAL_SPMV=sym|full|staged.
 inline int spmv_mode() {
@@ -104,11 +153,6 @@ struct GrpScal {
 };
 
 void spmv_init_grids();
-bool spmv_sym_usable(const Bsr& S);
-void spmv_sym_prepare(const Bsr& S);
-// TMA-staged symmetric SpMV; sc != nullptr fuses p^T A p and alpha (DOT).  false = not usable.
-bool launch_spmv_sym(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,
-                     double* partials, unsigned* counter, PcgScal* sc);
 void spmv_prepare(const Bsr& S);
 void launch_spmv(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y);
 void launch_spmv_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y,

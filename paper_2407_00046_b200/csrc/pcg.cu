@@ -66,13 +66,25 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
   cudaStream_t st = c->cap_stream;
   const int N = c->N;
   cudaEvent_t* ev = c->ev + set * (2 * kBatch + 1);
-  const int fg = pcg_fused_grid(N);  // occupancy query before the capture starts
+  const bool cg = ts_usable(S);
+  const int fg = cg ? 0 : pcg_fused_grid(N);  // occupancy query before the capture starts
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   for (int it = 0; it < kBatch; ++it) {
     // CUDA events bracket the first SpMV launch of every batch (a 1-in-kBatch live sample, so the
     // event nodes do not add gaps to every iteration): the bench reports the SpMV kernel's average
     // duration inside the timed region from these (roofline achieved GB/s)
+    if (cg) {
+      // Chronopoulos-Gear: update k (x, r, u, p, s) then SpMV k+1 (w = A u, the iteration's one
+      // grid-wide reduction, App. B stop test, alpha / beta)
+      launch_cg_update(st, N, c->dinv.ptr, S.ts->pin_ptr, S.ts->part, c->pq.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr,
+                       c->px.ptr, c->pr.ptr, c->upart.ptr, c->scal.ptr);
+      if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
+      launch_spmv_ts_dot(st, S, C, c->pz.ptr, c->pq.ptr, S.ts->part, c->dpart.ptr, c->counter.ptr, c->scal.ptr,
+                         c->upart.ptr, c->hist.ptr);
+      if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it + 1], st, cudaEventRecordExternal));
+      continue;
+    }
     if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
     launch_spmv_dot(st, S, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, c->scal.ptr);
     if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it + 1], st, cudaEventRecordExternal));
@@ -104,7 +116,7 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
   int k_prev = c->h_scal->k;
   CK(cudaGraphLaunch(ge[0], st));
   CK(cudaGraphLaunch(ge[1], st));
-  const int per_iter = pcg_fused_grid(c->N) > 0 ? 2 : 3;
+  const int per_iter = (ts_usable(S) || pcg_fused_grid(c->N) > 0) ? 2 : 3;
   c->launches += 2 * per_iter * kBatch;
   int cur = 0;
   while (true) {
@@ -211,9 +223,18 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.hcap = hcap;
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
-  launch_pcg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->partials.ptr, c->counter.ptr,
-                  c->scal.ptr, c->hist.ptr);
-  c->launches += 2;
+  if (ts_usable(S)) {
+    // single-reduction (Chronopoulos-Gear) PCG: init, then SpMV 0 (w_0 = A u_0, stop test at k = 0)
+    launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
+                   c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+    launch_spmv_ts_dot(st, S, C, c->pz.ptr, c->pq.ptr, S.ts->part, c->dpart.ptr, c->counter.ptr, c->scal.ptr,
+                       c->upart.ptr, c->hist.ptr);
+    c->launches += 3 + (S.ts ? 1 : 0);
+  } else {
+    launch_pcg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->partials.ptr,
+                    c->counter.ptr, c->scal.ptr, c->hist.ptr);
+    c->launches += 2;
+  }
   CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int ws_it = stats ? stats->ws_iters_max : 0, ng = stats ? stats->n_groups : 0;

@@ -380,14 +380,17 @@ void build_plan(bal_ctx* c) {
   halo_plan_build(c->N, d.adj_ptr.data(), d.adj_col.data(), hc ? crp.data() : nullptr, hc ? ccol.data() : nullptr,
                   d.world, d.bounds.data(), d.rank, d.plan);
   const size_t ns = d.plan.send_idx.size(), nr = d.plan.recv_idx.size();
-  d.send_idx.upload(d.plan.send_idx.data(), std::max<size_t>(ns, 1), c->st);
-  d.recv_idx.upload(d.plan.recv_idx.data(), std::max<size_t>(nr, 1), c->st);
+  d.send_idx.reserve(std::max<size_t>(ns, 1));
+  d.recv_idx.reserve(std::max<size_t>(nr, 1));
+  if (ns) d.send_idx.upload(d.plan.send_idx.data(), ns, c->st);
+  if (nr) d.recv_idx.upload(d.plan.recv_idx.data(), nr, c->st);
   d.sbuf.reserve(3 * std::max<size_t>(ns, 1));
   d.rbuf.reserve(3 * std::max<size_t>(nr, 1));
 }
 
 Bsr owned(const Bsr& S, const DistState& d) {
   Bsr b = S;
+  b.ts = nullptr;  // row-range (generic) kernel on every rank: SpMV bits independent of the partition
   b.r0 = d.r0;
   b.r1 = d.r1;
   return b;
@@ -424,7 +427,7 @@ void dist_init(bal_ctx* c, const bal_dist* dd) {
   if (bal_partition_rows(N, cost.data(), d.world, d.bounds.data()) != BAL_OK)
     throw std::invalid_argument("bal_init: partition failed");
   for (int k = 1; k < d.world; ++k) {
-    const int b = (int)(((long long)d.bounds[k] + kSymR / 2) / kSymR * kSymR);
+    const int b = (int)(((long long)d.bounds[k] + kPartAlign / 2) / kPartAlign * kPartAlign);
     d.bounds[k] = std::max(d.bounds[k - 1], std::min(b, N));
   }
   d.bounds[d.world] = N;

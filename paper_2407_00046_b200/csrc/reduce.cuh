@@ -76,6 +76,27 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
   }
 }
 
+// Chronopoulos-Gear (single-reduction) PCG scalars, set by the last CTA of the SpMV kernel of
+// iteration k (k_spmv_ts.cu) from gam = (r_k, u_k), rr = (r_k, r_k), delta = (A u_k, u_k), u = M^-1 r:
+// App. B stop test on ||r_k|| (same order as pcg_stop_check for the textbook recurrences), then
+// beta_k = gam_k / gam_{k-1}, alpha_k = gam_k / (delta_k - beta_k gam_k / alpha_{k-1}) -- computed
+// even when the solve stops, so an App. B resume continues with the update of step k.  The CG
+// objective decreases by alpha_{k-1} gam_{k-1} / 2 in step k-1 (R-PCG1 bookkeeping).
+BAL_D void cg_scalars(PcgScal* sc, double* hist, double gam, double rr, double delta) {
+  const int k = sc->k;
+  if (k > 0) sc->dec += 0.5 * sc->alpha * sc->rz;
+  sc->rr = rr;
+  hist[k] = sqrt(rr);
+  hist[sc->hcap + k] = sc->dec;
+  pcg_stop_check(sc, hist);
+  const double beta = (k > 0 && sc->rz != 0.0) ? gam / sc->rz : 0.0;
+  const double den = (k > 0 && sc->alpha != 0.0) ? delta - beta * gam / sc->alpha : delta;
+  sc->beta = beta;
+  sc->pq = den;
+  sc->alpha = (den != 0.0) ? gam / den : 0.0;  // r = 0 exactly: converged, the stop test fired
+  sc->rz = gam;
+}
+
 template <int NQ>
 BAL_D void grp_warp_accum(int g, const double (&v)[NQ], double* bucket /*[warps][kMaxGroups][NQ]*/) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -98,7 +98,7 @@ def test_spmv_every_row_and_pcg_iterations(assembled):
     Dinv = dinv_full(_np(out["diag_inv"]))
     xg = torch.empty(A.shape[0], dtype=torch.float64, device=DEV)
     s = bal.bal_pcg(ctx, _t(b), _t(np.zeros_like(b)), xg, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=10)
-    st = la.pcg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=10)
+    st = la.pcg_cg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=10)
     assert s["iters"] == 10 == st.k
     assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x), name
 

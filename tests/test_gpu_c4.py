@@ -111,16 +111,37 @@ def test_c4_spmv_every_row(c4):
 
 
 def test_c4_pcg_fixed_iterations(c4):
-    """k textbook block-Jacobi PCG iterations (no stopping) from x0 = 0 on the assembled C4 system."""
+    """k block-Jacobi PCG iterations (no stopping) from x0 = 0 on the assembled C4 system: the GPU's
+    single-reduction (Chronopoulos-Gear) PCG against the oracle's pcg_cg (1e-10) and the textbook
+    recurrences (1e-8)."""
     sc, m, x, y, ctx, out, A = c4
     b = -_np(out["grad"])
     Dinv = dinv_full(_np(out["diag_inv"]))
     xg = torch.empty(A.shape[0], dtype=torch.float64, device=DEV)
-    k = 12
+    k = 50
     s = bal.bal_pcg(ctx, _t(b), _t(np.zeros_like(b)), xg, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=k)
-    st = la.pcg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+    st = la.pcg_cg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
     assert s["iters"] == k == st.k
     assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
+    tb = la.pcg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+    assert np.linalg.norm(_np(xg) - tb.x) <= 1e-8 * np.linalg.norm(tb.x)
+
+
+def test_c4_pcg_to_app_b_stop(c4):
+    """A full solve on the C4 system under the App. B policy (Q14, R-PCG1): the GPU stops
+    converged with ||b - A x|| <= 1e-4 ||b|| recomputed on the CPU from the returned x, or stagnated
+    with the CG objective phi(x) = x'Ax/2 - b'x below phi(0) = 0 (a descent direction)."""
+    sc, m, x, y, ctx, out, A = c4
+    b = -_np(out["grad"])
+    xg = torch.empty(A.shape[0], dtype=torch.float64, device=DEV)
+    s = bal.bal_pcg(ctx, _t(b), _t(np.zeros_like(b)), xg, warm_start=0)
+    xs = _np(xg)
+    r = b - A @ xs
+    assert s["stop_reason"] in (0, 1), s
+    if s["stop_reason"] == 0:
+        assert np.linalg.norm(r) <= 1.0001e-4 * np.linalg.norm(b)
+    assert 0.5 * xs @ (A @ xs) - b @ xs < 0.0
+    assert abs(np.linalg.norm(r) / np.linalg.norm(b) - s["rel_residual"]) <= 1e-6 * max(s["rel_residual"], 1e-4)
 
 
 @pytest.fixture(scope="module")

@@ -73,7 +73,10 @@ def test_spmv_rows_partition_is_bitwise_identical():
     bal.bal_assemble(ctx, xt, y=sc["x0"] + 0.01 * rng.normal(size=sc["x0"].shape))
     v = torch.as_tensor(rng.normal(size=3 * N), device=DEV)
     y = torch.empty_like(v)
-    bal.bal_spmv(ctx, v, y)
+    bal.bal_spmv_rows(ctx, 0, N, v, y)  # the partitioned path's row-range kernel, one part
+    yt = torch.empty_like(v)
+    bal.bal_spmv(ctx, v, yt)  # single-GPU tile-symmetric kernel: same product, other summation order
+    assert torch.allclose(yt, y, rtol=1e-12, atol=1e-12 * float(y.abs().max()))
     for parts in (2, 3, 7):
         cuts = sorted({min(N, SYM_R * int(round(k * N / parts / SYM_R))) for k in range(1, parts)} | {0, N})
         yp = torch.full_like(v, float("nan"))

@@ -164,6 +164,27 @@ def test_spmv_on_gpu_assembled_system(cubes_state):
     assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)
 
 
+@pytest.mark.parametrize("budget", [24, 96, 333])
+def test_spmv_tile_budgets_on_oracle_system(cubes_state, budget, monkeypatch):
+    """The tile-symmetric SpMV (k_spmv_ts) for several tile sizes (more tiles = more cross-tile
+    partials, single-row tiles at 24): element-wise parity with the oracle's product and bitwise
+    equality of repeated products."""
+    monkeypatch.setenv("BAL_TS_BUDGET", str(budget))
+    sc, o, x1, _ = cubes_state
+    pt, ee = cm.candidates(o.mesh, x1, x1, o.dhat)
+    keys, d = cm.constraint_set(x1, pt, ee, o.dhat)
+    A = o.assemble(x1, oracle_state(o, x1, sigma=4e5), keys)["A"]
+    ctx = bal.bal_init(sc)
+    bal.bal_load_bsr(ctx, *csr_to_bsr(A, o.N))
+    v = np.random.default_rng(10 + budget).normal(size=3 * o.N)
+    yg = torch.empty(3 * o.N, dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)
+    y2 = torch.empty_like(yg)
+    bal.bal_spmv(ctx, _t(v), y2)
+    assert torch.equal(yg, y2)
+
+
 # --------------------------------------------------------------------------- PCG (a8, a9)
 def _loaded_system(cubes_state):
     sc, o, x1, _ = cubes_state
@@ -186,9 +207,13 @@ def test_pcg_fixed_iterates_and_converged_parity(cubes_state):
     for k in (1, 5, 20):
         s = bal.bal_pcg(ctx, _t(b), _t(np.zeros(3 * N)), xg, warm_start=0, rel_tol=0.0, stall_window=0,
                         max_iters=k)
-        st = la.pcg(A, b, np.zeros(3 * N), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+        st = la.pcg_cg(A, b, np.zeros(3 * N), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
         assert s["iters"] == k == st.k
         assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
+        tb = la.pcg(A, b, np.zeros(3 * N), Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+        assert np.linalg.norm(_np(xg) - tb.x) <= 1e-8 * np.linalg.norm(tb.x)
+        hg = bal.bal_pcg_history(ctx, k + 1)
+        assert np.max(np.abs(hg - np.asarray(st.hist))) <= 1e-10 * st.hist[0]
     # (ii) converged to 1e-12: vs oracle and vs a direct solve
     s = bal.bal_pcg(ctx, _t(b), None, xg, warm_start=0, rel_tol=1e-12, stall_window=0, max_iters=20000)
     xd = np.linalg.solve(A.toarray(), b)
@@ -196,7 +221,7 @@ def test_pcg_fixed_iterates_and_converged_parity(cubes_state):
     assert np.linalg.norm(_np(xg) - xd) <= 1e-8 * np.linalg.norm(xd)
     # (iii) App. B default policy: same iteration count and stop reason as the oracle
     s = bal.bal_pcg(ctx, _t(b), None, xg, warm_start=0)
-    st = la.pcg(A, b, np.zeros(3 * N), Dinv, tol=1e-4, window=100, max_iters=20000)
+    st = la.pcg_cg(A, b, np.zeros(3 * N), Dinv, tol=1e-4, window=100, max_iters=20000)
     assert s["stop_reason"] == st.stop
     assert abs(s["iters"] - st.k) <= 1
     r = b - A @ _np(xg)

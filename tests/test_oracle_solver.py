@@ -163,6 +163,37 @@ def test_pcg_special_cases_and_dense_solve():
     assert s2.stop == la.STOP_STAGNATED
 
 
+def test_pcg_chronopoulos_gear_special_cases_and_textbook_iterates():
+    """pcg_cg (the GPU's single-reduction form) against closed forms and the textbook recurrences:
+    identity -> 1 iteration; 3 distinct eigenvalues -> <= 3 iterations; dense solve; and for k <= 20
+    the same iterates as Saad Alg. 9.1 (the two are equal in exact arithmetic)."""
+    rng = np.random.default_rng(26)
+    import scipy.sparse as sp
+    N = 10
+    Dinv = np.tile(np.eye(3), (N, 1, 1))
+    b = rng.normal(size=3 * N)
+    st = la.pcg_cg(sp.identity(3 * N, format="csr"), b, np.zeros(3 * N), Dinv, tol=1e-12)
+    assert st.k == 1 and np.allclose(st.x, b)
+    dg = np.repeat([1.0, 2.0, 3.0], N)
+    st = la.pcg_cg(sp.diags(dg).tocsr(), b, np.zeros(3 * N), Dinv, tol=1e-12)
+    assert st.k <= 3 and np.allclose(st.x, b / dg, rtol=1e-10)
+    bs = _rand_spd_blocks(rng, 25, cond_scale=1e3)
+    A = bs.to_csr()
+    Dinv = np.linalg.inv(bs.diag_blocks())
+    b = rng.normal(size=75)
+    xd = np.linalg.solve(bs.to_dense(), b)
+    st = la.pcg_cg(A, b, np.zeros(75), Dinv, tol=1e-13, window=10 ** 9)
+    assert np.linalg.norm(st.x - xd) <= 1e-9 * np.linalg.norm(xd)
+    x0 = rng.normal(size=75)
+    for k in (1, 2, 5, 10, 20):
+        a = la.pcg_cg(A, b, x0, Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+        t = la.pcg(A, b, x0, Dinv, tol=0.0, window=10 ** 9, max_iters=k)
+        assert a.k == t.k == k
+        assert np.linalg.norm(a.x - t.x) <= 1e-10 * np.linalg.norm(t.x)
+        assert np.max(np.abs(np.subtract(a.hist, t.hist))) <= 1e-10 * t.hist[0]
+        assert np.max(np.abs(np.subtract(a.dec, t.dec))) <= 1e-10 * t.dec[-1]
+
+
 def test_warm_start_exact_on_decoupled_groups():
     rng = np.random.default_rng(25)
     b1 = _rand_spd_blocks(rng, 8)
