@@ -698,6 +698,79 @@ void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, 
   CK(cudaGetLastError());
 }
 
+// Two nodes per thread: their 6 consecutive doubles of every vector and 12 of D^-1 are read and
+// written as 16-byte vectors (node pairs start 48 B apart, so every access is 16-byte aligned).
+template <int NP>
+BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* __restrict__ pin_ptr,
+                           const double* __restrict__ part, const double* __restrict__ w, double* __restrict__ u,
+                           double* __restrict__ p, double* __restrict__ s, double* __restrict__ x,
+                           double* __restrict__ r, double alpha, double beta, double& g, double& rr) {
+  constexpr int ND = 3 * NP;
+  const size_t d0 = 3 * (size_t)i0;
+  double wv[ND], uv[ND], pv[ND], sv[ND], xv[ND], rv[ND];
+  if (NP == 2) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double2 a = reinterpret_cast<const double2*>(w + d0)[k];
+      const double2 b = reinterpret_cast<const double2*>(u + d0)[k];
+      const double2 c = reinterpret_cast<const double2*>(p + d0)[k];
+      const double2 d = reinterpret_cast<const double2*>(s + d0)[k];
+      const double2 e = reinterpret_cast<const double2*>(x + d0)[k];
+      const double2 f = reinterpret_cast<const double2*>(r + d0)[k];
+      wv[2 * k] = a.x; wv[2 * k + 1] = a.y;
+      uv[2 * k] = b.x; uv[2 * k + 1] = b.y;
+      pv[2 * k] = c.x; pv[2 * k + 1] = c.y;
+      sv[2 * k] = d.x; sv[2 * k + 1] = d.y;
+      xv[2 * k] = e.x; xv[2 * k + 1] = e.y;
+      rv[2 * k] = f.x; rv[2 * k + 1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      wv[k] = w[d0 + k]; uv[k] = u[d0 + k]; pv[k] = p[d0 + k];
+      sv[k] = s[d0 + k]; xv[k] = x[d0 + k]; rv[k] = r[d0 + k];
+    }
+  }
+  if (pin_ptr) {
+#pragma unroll
+    for (int n = 0; n < NP; ++n) {
+      const int e0 = pin_ptr[i0 + n], e1 = pin_ptr[i0 + n + 1];
+      for (int e = e0; e < e1; ++e) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) wv[3 * n + c] += part[3 * (size_t)e + c];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < ND; ++k) {
+    pv[k] = uv[k] + beta * pv[k];
+    sv[k] = wv[k] + beta * sv[k];
+    xv[k] = xv[k] + alpha * pv[k];
+    rv[k] = rv[k] - alpha * sv[k];
+  }
+#pragma unroll
+  for (int n = 0; n < NP; ++n) {
+    dinv_apply(dinv, i0 + n, rv[3 * n], rv[3 * n + 1], rv[3 * n + 2], uv[3 * n], uv[3 * n + 1], uv[3 * n + 2]);
+    g += rv[3 * n] * uv[3 * n] + rv[3 * n + 1] * uv[3 * n + 1] + rv[3 * n + 2] * uv[3 * n + 2];
+    rr += rv[3 * n] * rv[3 * n] + rv[3 * n + 1] * rv[3 * n + 1] + rv[3 * n + 2] * rv[3 * n + 2];
+  }
+  if (NP == 2) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      reinterpret_cast<double2*>(p + d0)[k] = make_double2(pv[2 * k], pv[2 * k + 1]);
+      reinterpret_cast<double2*>(s + d0)[k] = make_double2(sv[2 * k], sv[2 * k + 1]);
+      reinterpret_cast<double2*>(x + d0)[k] = make_double2(xv[2 * k], xv[2 * k + 1]);
+      reinterpret_cast<double2*>(r + d0)[k] = make_double2(rv[2 * k], rv[2 * k + 1]);
+      reinterpret_cast<double2*>(u + d0)[k] = make_double2(uv[2 * k], uv[2 * k + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      p[d0 + k] = pv[k]; s[d0 + k] = sv[k]; x[d0 + k] = xv[k]; r[d0 + k] = rv[k]; u[d0 + k] = uv[k];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kVecThreads)
 k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_ptr, const double* __restrict__ part,
             const double* __restrict__ w, double* __restrict__ u, double* __restrict__ p, double* __restrict__ s,
@@ -705,36 +778,17 @@ k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_
   if (sc->done) return;
   const double alpha = sc->alpha, beta = sc->beta;
   double g = 0.0, rr = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    double wi[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) wi[c] = w[3 * (size_t)i + c];
-    if (pin_ptr) {
-      const int e0 = pin_ptr[i], e1 = pin_ptr[i + 1];
-      for (int e = e0; e < e1; ++e) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) wi[c] += part[3 * (size_t)e + c];
-      }
-    }
-    double rv[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const size_t j = 3 * (size_t)i + c;
-      const double pj = u[j] + beta * p[j];
-      const double sj = wi[c] + beta * s[j];
-      p[j] = pj;
-      s[j] = sj;
-      x[j] = x[j] + alpha * pj;
-      rv[c] = r[j] - alpha * sj;
-      r[j] = rv[c];
-    }
-    double u0, u1, u2;
-    dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
-    u[3 * (size_t)i] = u0;
-    u[3 * (size_t)i + 1] = u1;
-    u[3 * (size_t)i + 2] = u2;
-    g += rv[0] * u0 + rv[1] * u1 + rv[2] * u2;
-    rr += rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2];
+  // 16-byte alignment of every vector (cudaMalloc / torch allocations); else one node per thread
+  const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(p) |
+                     reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r)) &
+                    15) == 0;
+  const int T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const int npairs = n / 2;
+    for (int q = t; q < npairs; q += T) cg_update_nodes<2>(2 * q, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
+    if ((n & 1) && t == T - 1) cg_update_nodes<1>(n - 1, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
+  } else {
+    for (int i = t; i < n; i += T) cg_update_nodes<1>(i, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
   }
   __shared__ double sh[kVecThreads / 32];
   const double bg = block_sum<kVecThreads>(g, sh);

@@ -367,13 +367,17 @@ def spiky_ball_occ(R, n_spikes, spike_len, spike_r=0.75):
 
 def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=20.4, n_spikes=110,
                     spike_len=15.0, n_balls=4, E_ball=5e5, E_net=1e9, nu=0.4, rho=1e3, chi=0.3, drop_gap=0.002,
-                    jitter_deg=(0.2, 0.8)):
+                    jitter_deg=(0.2, 0.8), settled=False, rest_gap=(0.4e-3, 0.7e-3)):
     """C4 recipe (Table 1 row 1 P:664 for the statistics): a chain-net of
     interlocked 1-voxel-thick square rings (horizontal rings on an nx x nz lattice plus vertical
     connector rings threading neighbours through their holes; outermost horizontal rings fixed)
     and n_balls spiky balls (voxel core + radial spikes on a Fibonacci direction set) dropped onto
     it.  Every ring gets a small generic rotation so no cross-body edges are exactly parallel.
-    Defaults target T ~ 1.76M tets, N ~ 0.8M nodes."""
+    Defaults target T ~ 1.76M tets, N ~ 0.8M nodes.
+    settled=True: the contact-rich start the paper's statistics describe (228K avg constraints,
+    P:664): every connector ring hangs on the two rings it threads (its top beam rests on their
+    beams with a clearance drawn from rest_gap, below d_hat) and the balls start rest_gap above the
+    net; rotations are reduced to 0.05-0.1 deg so the clearances stay positive."""
     rng = np.random.default_rng(seed)
     sb = SceneBuilder()
     assert L == 8 and spacing == 10, "connector layout below is laid out for L=8, spacing=10"
@@ -386,12 +390,25 @@ def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=20
     xcx, tcx = voxel_mesh(_ring_xy(conn_len, 9), voxel)
     xcz, tcz = voxel_mesh(_ring_zy(conn_len, 9), voxel)
 
+    if settled:
+        jitter_deg = (0.05, 0.1)
+
     def jitter(x):
         c = x.mean(0)
         ax = rng.normal(size=3)
         R = rot_axis(ax, np.deg2rad(rng.uniform(*jitter_deg)))
         return (x - c) @ R.T + c
 
+    def hang(xc, host_top):
+        """settled: lower a connector so its top beam rests rest_gap above the host beams' top."""
+        if not settled:
+            return xc
+        top_beam = xc[:, 1] > xc[:, 1].max() - 1.5 * voxel
+        return xc - np.array([0.0, xc[top_beam, 1].min() - host_top - rng.uniform(*rest_gap), 0.0])
+
+    # bodies in the original interleaved order (ring, x-connector, z-connector per lattice site; the
+    # node numbering and the rotation draws of the default scene are unchanged by `settled`)
+    bodies, tops = [], {}
     for i in range(nx):
         for k in range(nz):
             o = np.array([i * spacing, 0.0, k * spacing]) * voxel
@@ -399,19 +416,27 @@ def make_puffer_net(seed=4, nx=40, nz=40, L=8, spacing=10, voxel=0.01, ball_R=20
             x = xr + o
             if not border:
                 x = jitter(x)
-            sb.add_body(x, tr, 1, fixed=np.full(len(xr), 1 if border else 0, np.uint8))
+            tops[i, k] = float(x[:, 1].max())
+            bodies.append(("ring", x, tr, np.full(len(xr), 1 if border else 0, np.uint8), None))
             if i + 1 < nx:
                 # vertical ring in the xy plane through the holes of rings (i,k) and (i+1,k)
                 oc = o + np.array([4.5, -4.0, 4.5]) * voxel
-                sb.add_body(jitter(xcx + oc), tcx, 1)
+                bodies.append(("conn", jitter(xcx + oc), tcx, None, ((i, k), (i + 1, k))))
             if k + 1 < nz:
                 oc = o + np.array([3.0, -4.0, 4.5]) * voxel
-                sb.add_body(jitter(xcz + oc), tcz, 1)
+                bodies.append(("conn", jitter(xcz + oc), tcz, None, ((i, k), (i, k + 1))))
+    for kind, x, t, fx, hosts in bodies:
+        if kind == "conn":
+            x = hang(x, max(tops[hosts[0]], tops[hosts[1]]))
+        sb.add_body(x, t, 1, fixed=fx)
     occ, ext = spiky_ball_occ(ball_R, n_spikes, spike_len)
     xb, tb = voxel_mesh(occ, voxel)
     xb = xb - ext * voxel
     span = np.array([(nx - 1) * spacing + L, (nz - 1) * spacing + L]) * voxel
     top = 6 * voxel  # above the connector rings
+    if settled:  # balls rest_gap above the highest point of the net (the hanging connectors' tops)
+        top = max(float(b_x[:, 1].max()) for b_x in sb.x)
+        drop_gap = rest_gap[0]
     for b in range(n_balls):
         fx = (0.3 + 0.4 * (b % 2)) * span[0]
         fz = (0.3 + 0.4 * (b // 2 % 2)) * span[1]
