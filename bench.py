@@ -2,7 +2,9 @@
 """Benchmark of the BAL inexact Newton-PCG time step (arXiv 2407.00046) on B200.
 
 Metric (BASELINE.json): "seconds/frame & PCG iters/s at 1.76M tets; BSR SpMV HBM GB/s vs peak".
-Workload: the C4 puffer-balls-on-chain-net scene (configs[3], ~1.75M tets, dt = 1/30 s).  A C4
+Workload: the C4 puffer-balls-on-chain-net scene (configs[3], ~1.75M tets, dt = 1/30 s) in its
+contact-rich start (scenes.make_puffer_net(settled=True): connectors hanging on the net, balls
+resting above it; ~2.6e5 active constraints, the paper's 228K avg / 292K max).  A C4
 frame takes hundreds of inexact-Newton iterations of thousands of PCG iterations each (the paper
 reports 156.8 Newton iterations and 427 s per frame on its GPU), so one bench step is ONE
 inexact-Newton iteration of Alg. 1 -- every row of SURVEY §8(a) once: constraint sets, elastic /
@@ -13,7 +15,12 @@ ranks each advance their own replica: weak scaling, no data-path collective).  S
 are reported when a frame completes inside the timed region, and as ms/Newton x the Newton
 iterations per frame of a recorded long run (profiles/c4_frames.json) otherwise, labelled so.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c4-drop|c1|c5]
+
+Headline fields of the line: ms_per_newton (all phases of one Newton iteration), the active
+constraint counts of the timed iterations, and seconds_per_frame when a frame completes inside the
+timed region (else the whole-frame runs measured separately, cited by file).  `value` (PCG iters/s
+over whole Newton iterations) is the metric's second component.
 """
 from __future__ import annotations
 
@@ -32,9 +39,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "seconds/frame & PCG iters/s at 1.76M tets; BSR SpMV HBM GB/s vs peak"
 UNIT = "PCG iters/s"
-# PCG iterations per Newton iteration observed on the GPU path on C4 (gpurun_out probe runs, round 1);
-# used only to size the reference (oracle) arm's step.
-C4_PCG_PER_NEWTON = 6000.0
+# PCG iterations per Newton iteration of the GPU path on the bench workload, read from the last
+# committed bench line (profiles/bench_r02_c4.json) so the reference (oracle) arm's step does the
+# same work; fallback: the App. B cap the contact-rich start hits (20,000)
+C4_PCG_PER_NEWTON_FALLBACK = 20000.0
 
 
 def parse():
@@ -43,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c4", "c4-drop", "c1", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -55,7 +63,19 @@ def make_scene(cfg):
         return scenes.make_cubes(1), "C1 two stacked soft cubes (1.5K tets), dt=1/30 s"
     if cfg == "c5":
         return scenes.make_puffer_tiles(5), "C5 3x2 replicated puffer-net tiles (~10.5M tets) on ONE GPU, dt=1/30 s"
-    return scenes.make_puffer_net(seed=4), "C4 puffer balls on chain-net (~1.7M tets), dt=1/30 s"
+    if cfg == "c4-drop":
+        return scenes.make_puffer_net(seed=4), "C4 puffer balls dropped on chain-net (~1.7M tets, few contacts), dt=1/30 s"
+    return (scenes.make_puffer_net(seed=4, settled=True),
+            "C4 puffer balls on chain-net, contact-rich start (~1.7M tets, ~2.6e5 constraints), dt=1/30 s")
+
+
+def gpu_pcg_per_newton(cfg):
+    f = os.path.join(ROOT, "profiles", f"bench_r02_{cfg}.json")
+    try:
+        with open(f) as fh:
+            return float(json.load(fh)["pcg_iters_per_newton"]), f"GPU run's mean ({os.path.relpath(f, ROOT)})"
+    except Exception:  # noqa: BLE001
+        return C4_PCG_PER_NEWTON_FALLBACK, "App. B cap (no committed GPU line)"
 
 
 class ClockSampler:
@@ -189,7 +209,7 @@ def run_reference(args):
     if rank != 0:
         return
     sc, wl = make_scene(args.config)
-    ppn = C4_PCG_PER_NEWTON if args.config == "c4" else 100.0
+    ppn, ppn_src = gpu_pcg_per_newton(args.config) if args.config.startswith("c4") else (100.0, "fixed")
     vals = []
     t_all = time.perf_counter()
     info = {}
@@ -207,7 +227,8 @@ def run_reference(args):
             "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
                        "step": "one inexact-Newton iteration of Alg. 1"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": desc + f"; one step = assembly + {ppn:.0f} PCG iterations (extrapolated)"},
+                             "sample": desc + f"; one step = assembly + {ppn:.0f} PCG iterations ({ppn_src}), "
+                                              f"extrapolated"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "detail": {**info, "wall_s": time.perf_counter() - t_all}}
     print(json.dumps(line), flush=True)
@@ -228,6 +249,7 @@ class FrameRunner:
                      "ms_pcg": 0.0, "ms_linesearch": 0.0, "max_constraints": 0}
         self.frames = []  # (ms_total, newton_iters, pcg_iters) of completed frames
         self.unconverged = 0
+        self.nA = []  # |A| of every Newton iteration run (decision trace)
         bal.bal_frame_begin(ctx, self.x, self.v)
 
     def totals(self):
@@ -248,6 +270,9 @@ class FrameRunner:
                 raise
             self.unconverged += 1
             conv = True
+        tr = self.bal.bal_get_trace(self.ctx, max_records=4096)
+        if tr:
+            self.nA.append(int(tr[-1]["nA"]))
         if conv:
             st = self.bal.bal_frame_finish(self.ctx, self.xn, self.vn, allow_unconverged=True)
             for k in self.done:
@@ -284,6 +309,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     spmv0 = bal.bal_spmv_counters(ctx)
+    nA0 = len(run.nA)
     launches0 = ctx.kernel_launches
     tot0 = run.totals()
     nf0 = len(run.frames)
@@ -319,11 +345,14 @@ def run_ours(args):
     spmv_us = 1000.0 * d_ms / max(d_n, 1)
     achieved = (d_alg / max(d_n, 1)) / (spmv_us * 1e-6) / 1e9 if d_n else None
     moved_gbs = (d_mov / max(d_n, 1)) / (spmv_us * 1e-6) / 1e9 if d_n else None
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    # ncu DRAM bytes per launch of the SpMV on this workload (one `ncu --set full` capture, committed
+    # per config under profiles/; null when none was taken for this config)
+    traffic, traffic_src = None, None
+    tf = os.path.join(ROOT, "profiles", f"spmv_traffic_{args.config}.json")
     if os.path.exists(tf):
         with open(tf) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
+        traffic_src = os.path.relpath(tf, ROOT)
     # SURVEY d.1 (b): PCG microbenchmark on the live (last assembled) C4 system: 1,000 global PCG
     # iterations, termination disabled, CUDA events (outside the timed region)
     pcg_micro = None
@@ -341,37 +370,31 @@ def run_ours(args):
                      "iters_per_s": 1000.0 * sm["iters"] / m0.elapsed_time(m1)}
     except Exception as ex:  # noqa: BLE001 -- reported, never fatal for the main line
         pcg_micro = {"error": str(ex)}
-    # e2e through the public API with host buffers: pinned x_t, v_t -> device, the same number of
-    # Newton iterations of a frame, x back to the host, all inside the timed region
+    # e2e through the public C ABI with HOST buffers: bal_step_host (x_t, v_t host -> device, the
+    # time step, x_{t+1}, v_{t+1} device -> host inside the call) on a context whose Newton cap is
+    # E2E_NEWTON iterations (BAL_E_NOT_CONVERGED returns the last accepted iterate and the stats),
+    # timed on the host around the call
     e2e = None
     if not args.no_e2e:
-        xh = x.detach().cpu().pin_memory()
-        vh = v.detach().cpu().pin_memory()
-        xo = torch.empty_like(xh).pin_memory()
-        ne = max(1, min(args.steps, 3))
-        xd, vd, xnd = torch.empty_like(x), torch.empty_like(v), torch.empty_like(x)
+        E2E_NEWTON = 2
+        prm = dict(sc["params"])
+        prm["max_newton"] = E2E_NEWTON
+        ctx2 = bal.bal_init(sc, device=local, params=prm)
+        xh = run.x.detach().cpu().numpy().copy()
+        vh = run.v.detach().cpu().numpy().copy()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        xd.copy_(xh, non_blocking=True)
-        vd.copy_(vh, non_blocking=True)
-        bal.bal_frame_begin(ctx, xd, vd)
-        p0 = 0
-        conv = False
-        for _ in range(ne):
-            conv = bal.bal_frame_iterate(ctx, 1)
-            if conv:
-                break
-        pe = bal.bal_frame_stats(ctx)["pcg_iters"] - p0
-        bal.bal_frame_finish(ctx, xnd, None, allow_unconverged=True)  # x_next = last accepted iterate
-        xo.copy_(xnd, non_blocking=True)
-        torch.cuda.synchronize()
+        _xn, _vn, st2 = bal.bal_step_host(ctx2, xh, vh, allow_unconverged=True)
         el = time.perf_counter() - t0
-        _s, e2e_v = job_throughput(el, pe, world, dev)
+        _s, e2e_v = job_throughput(el, st2["pcg_iters"], world, dev)
         nb = 3 * 8 * len(sc["rest_x"])
-        e2e = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * nb / ne, "d2h_bytes_per_step": nb / ne,
-               "steps": ne, "note": "x_t, v_t H2D from pinned memory + frame setup + ne Newton iterations + x D2H"}
+        e2e = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
+               "newton_iters": st2["newton_iters"], "pcg_iters": st2["pcg_iters"], "seconds": el,
+               "note": f"bal_step_host (host x_t, v_t in; x_t+1, v_t+1 out) with the Newton cap at {E2E_NEWTON}, "
+                       "from the state the timed region ended in"}
+        del ctx2
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -385,18 +408,21 @@ def run_ours(args):
                "sample": desc + f"; one step = assembly + {ppn:.0f} PCG iterations (the GPU run's mean), "
                                 f"extrapolated"}
     ms_newton = ms_max / max(newton, 1)
+    nA_t = run.nA[nA0:]
+    # whole-frame runs of this workload measured separately (tools/c4_frames.py, committed under
+    # profiles/ as <config>_frames_r02*.json): measured seconds per frame, cited by file
+    import glob
     npf_ref = None
     long_runs = {}
-    for tag, fn in (("chi=0.3 (scene default)", f"{args.config}_frames.json"), ("chi=0", f"{args.config}_frames_chi0.json")):
-        rf = os.path.join(ROOT, "profiles", fn)
-        if os.path.exists(rf):
-            with open(rf) as f:
-                lr = json.load(f)
-            long_runs[tag] = {k: lr.get(k) for k in ("seconds_per_frame", "newton_per_frame", "frames_converged",
-                                                     "max_newton", "when")}
-            long_runs[tag]["file"] = "profiles/" + fn
-            if tag.startswith("chi=0.3"):
-                npf_ref = lr.get("newton_per_frame")
+    for rf in sorted(glob.glob(os.path.join(ROOT, "profiles", f"{args.config}_frames_r02*.json"))):
+        with open(rf) as f:
+            lr = json.load(f)
+        tag = os.path.basename(rf)[:-5]
+        long_runs[tag] = {k: lr.get(k) for k in ("seconds_per_frame", "newton_per_frame", "frames_converged",
+                                                 "frames", "chi", "max_newton", "when")}
+        long_runs[tag]["file"] = os.path.relpath(rf, ROOT)
+        if lr.get("frames_converged") and npf_ref is None:
+            npf_ref = lr.get("newton_per_frame")
     line = {
         "metric": METRIC, "value": pcg_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -406,6 +432,13 @@ def run_ours(args):
                            "start, PCG, CCD line search, AL updates); frames continue across steps",
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (system ~0.5 GB/PCG iteration)"},
+        "headline": {"ms_per_newton": ms_newton,
+                     "active_constraints": {"avg": float(np.mean(nA_t)) if nA_t else None,
+                                            "max": int(max(nA_t)) if nA_t else None,
+                                            "paper": "228K avg / 292K max (P:664)"},
+                     "seconds_per_frame": (float(np.mean([f[0] for f in new_frames])) / 1000.0) if new_frames else None,
+                     "seconds_per_frame_note": "frames completed inside the timed region; whole-frame runs: "
+                                               "whole_frame_runs"},
         "pcg_iters_per_s_in_pcg": pcg / (d["ms_pcg"] / 1000.0) if d["ms_pcg"] > 0 else None,
         "pcg_microbench": pcg_micro,
         "newton_iters": newton, "pcg_iters": pcg, "pcg_iters_per_newton": ppn,
@@ -416,11 +449,12 @@ def run_ours(args):
         "frames_hit_newton_cap": run.unconverged,
         "seconds_per_frame": (float(np.mean([f[0] for f in new_frames])) / 1000.0) if new_frames else None,
         "seconds_per_frame_projection": (ms_newton * npf_ref / 1000.0) if npf_ref else None,
-        "newton_per_frame_ref": npf_ref,
+        "newton_per_frame_ref": npf_ref,  # from a converged whole-frame run only (projection = ms/Newton x it)
         "whole_frame_runs": long_runs or None,
         "max_constraints": tot1["max_constraints"],
-        "roofline": {"kernel": "k_spmv (BSR3 SpMV in PCG)", "bound": "hbm", "achieved": achieved, "peak": peak,
+        "roofline": {"kernel": "k_spmv_ts (BSR3 SpMV in PCG)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": peak_src, "mean_launch_us": spmv_us, "launches": d_n,
                      "alg_bytes_per_launch": d_alg / max(d_n, 1), "kernel_min_bytes_per_launch": d_mov / max(d_n, 1),
                      "kernel_min_gbs": moved_gbs},

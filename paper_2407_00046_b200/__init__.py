@@ -227,16 +227,21 @@ def bal_frame_stats(ctx):
     return {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
 
 
-def bal_step_host(ctx, x_t, v_t):
-    """End-to-end step on host numpy arrays (copies inside the call)."""
+def bal_step_host(ctx, x_t, v_t, allow_unconverged=False):
+    """End-to-end step on host numpy arrays (copies inside the call).  allow_unconverged: return
+    the last accepted iterate and the stats on BAL_E_NOT_CONVERGED (stats["converged"] False)."""
     x_t = np.ascontiguousarray(x_t, np.float64).ravel()
     v_t = np.ascontiguousarray(v_t, np.float64).ravel()
     xn = np.empty_like(x_t)
     vn = np.empty_like(v_t)
     s = bal_step_stats()
-    _check(ctx, _lib.lib.bal_step_host(ctx.handle, _lib.ptr(x_t, C.c_double), _lib.ptr(v_t, C.c_double),
-                                       _lib.ptr(xn, C.c_double), _lib.ptr(vn, C.c_double), C.byref(s)))
-    return xn, vn, {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
+    st = _lib.lib.bal_step_host(ctx.handle, _lib.ptr(x_t, C.c_double), _lib.ptr(v_t, C.c_double),
+                                _lib.ptr(xn, C.c_double), _lib.ptr(vn, C.c_double), C.byref(s))
+    out = {f: getattr(s, f) for f, _ in bal_step_stats._fields_}
+    out["converged"] = st == 0
+    if not (st == -4 and allow_unconverged):
+        _check(ctx, st)
+    return xn, vn, out
 
 
 TRACE_FIELDS = ("l", "nA", "nAp", "rebuilt", "dmin", "sigma", "ws_iters", "pcg_iters", "pcg_stop", "alpha_ccd",

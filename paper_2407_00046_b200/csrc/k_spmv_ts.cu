@@ -259,7 +259,7 @@ bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol,
   P.stage_bytes = P.o_crp + up128((size_t)(P.cap_rows + 1) * 4);
   // + the row terms (cs) and transposed terms (tp) of a tile, double-buffered across tiles
   P.o_scratch = 128 + (size_t)kTsStages * P.stage_bytes;
-  P.smem = P.o_scratch + kTsScratchBufs * 24 * (size_t)(P.cap_cs + P.cap_tp);
+  P.smem = P.o_scratch + kTsScratchBufs * 24 * (size_t)(P.cap_cs + P.cap_tp + kTsContactCap);
   return true;
 }
 
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       const double* xv = reinterpret_cast<const double*>(S + a.P.o_xv);
       // double-buffered scratch: [nb][3] A v_j (row terms) then [noff][3] A^T v_i (slot order)
       double* cs = reinterpret_cast<double*>(sm + a.P.o_scratch) +
-                   (size_t)(it % kTsScratchBufs) * 3 * (a.P.cap_cs + a.P.cap_tp);
+                   (size_t)(it % kTsScratchBufs) * 3 * (a.P.cap_cs + a.P.cap_tp + kTsContactCap);
       double* tp = cs + 3 * (size_t)a.P.cap_cs;
       // ---- phase 1, one thread per stored block A_ij (i = r0 + il, j <= i): cs[q] = A v_j; an
       // off-diagonal block also writes A^T v_i to its slot tp[tslot[q]] (grouped by target row)
@@ -472,6 +472,25 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         }
       }
       TS_T(6)
+      // contact blocks of the tile's rows (one contiguous range of the row-sorted contact BSR): one
+      // thread per block, C_s v_col -> cc[s] (the first kTsContactCap of the tile; the rest, rare,
+      // are taken by their row thread in phase 2)
+      const int* cr = reinterpret_cast<const int*>(S + a.P.o_crp);
+      double* cc = tp + 3 * (size_t)a.P.cap_tp;
+      const int c0r = crp ? cr[0] : 0;
+      const int ncc = crp ? min(cr[R] - c0r, kTsContactCap) : 0;
+      for (int e = ct; e < ncc; e += kTsConsumers) {
+        const size_t s2 = (size_t)(c0r + e);
+        const double* A = a.C.val + 9 * s2;
+        const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
+        double m[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) m[k] = __ldg(A + k);
+        const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);
+        cc[3 * e] = fma(m[2], c2, fma(m[1], c1, m[0] * c0));
+        cc[3 * e + 1] = fma(m[5], c2, fma(m[4], c1, m[3] * c0));
+        cc[3 * e + 2] = fma(m[8], c2, fma(m[7], c1, m[6] * c0));
+      }
       bar_consumers();
       TS_T(1)
       // ---- phase 2, fixed-order sums, one thread per owned row il: stored blocks (ascending
@@ -483,8 +502,9 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         sum3(cs, M.rpc[il], M.rpc[il] + M.rle[il], acc0, acc1, acc2);
         sum3(tp, M.mps[il], M.mps[il] + M.mle[il], acc0, acc1, acc2);
         if (crp) {
-          const int* cr = reinterpret_cast<const int*>(S + a.P.o_crp);
-          for (int s2 = cr[il]; s2 < cr[il + 1]; ++s2) {
+          const int e0 = cr[il] - c0r, e1 = cr[il + 1] - c0r;
+          sum3(cc, e0, min(e1, ncc), acc0, acc1, acc2);
+          for (int s2 = c0r + max(e0, ncc); s2 < c0r + e1; ++s2) {
             const double* A = a.C.val + 9 * (size_t)s2;
             const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
             const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);

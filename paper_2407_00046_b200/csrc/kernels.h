@@ -35,7 +35,11 @@ constexpr int kTsStages = BAL_TS_STAGES;
 #ifndef BAL_TS_SCRATCH_BUFS
 #define BAL_TS_SCRATCH_BUFS 1
 #endif
-constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;  // 2: consecutive tiles' scratch double-buffered
+constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;
+#ifndef BAL_TS_CONTACT_CAP
+#define BAL_TS_CONTACT_CAP 384
+#endif
+constexpr int kTsContactCap = BAL_TS_CONTACT_CAP;  // contact blocks per tile computed block-parallel  // 2: consecutive tiles' scratch double-buffered
 constexpr int kTsMaxRows = kTsConsumers;  // one consumer thread per owned row
 
 constexpr int kElasticThreads = 128;

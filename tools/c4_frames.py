@@ -24,13 +24,17 @@ def main():
         kw["chi"] = float(sys.argv[sys.argv.index("--chi") + 1])
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join("profiles", "c4_frames.json")
     scene = sys.argv[sys.argv.index("--scene") + 1] if "--scene" in sys.argv else "c4"
-    make = {"c4": lambda: scenes.make_puffer_net(seed=4, **kw), "c2": lambda: scenes.make_armadillo_like(2, **kw),
+    make = {"c4": lambda: scenes.make_puffer_net(seed=4, **kw),
+            "c4s": lambda: scenes.make_puffer_net(seed=4, settled=True, **kw),
+            "c2": lambda: scenes.make_armadillo_like(2, **kw),
             "c3": lambda: scenes.make_impact(3, **kw), "c1": lambda: scenes.make_cubes(1)}[scene]
     sc = make()
     if "--max-newton" in sys.argv:
         sc["params"]["max_newton"] = int(sys.argv[sys.argv.index("--max-newton") + 1])
     dev = torch.device("cuda:0")
     flags = bal.BAL_FRICTION_LAGGED if "--lagged-friction" in sys.argv else 0
+    if "--no-freeze" in sys.argv:
+        flags |= bal.BAL_FRICTION_NO_FREEZE
     ctx = bal.bal_init(sc, flags=flags)
     st = torch.cuda.current_stream(dev)
     x = torch.as_tensor(sc["x0"].ravel(), device=dev)
@@ -57,13 +61,17 @@ def main():
         x, v = xn, vn
     conv = [fr for fr in frames if fr["converged"]]
     res = {"scene": sc["name"] + "".join(f", {k}={v}" for k, v in kw.items())
-                    + (" with BAL_FRICTION_LAGGED" if flags else ""), "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
+                    + (" with BAL_FRICTION_LAGGED" if flags & bal.BAL_FRICTION_LAGGED else "")
+                    + (" with BAL_FRICTION_NO_FREEZE" if flags & bal.BAL_FRICTION_NO_FREEZE else ""),
+           "chi": float(sc["params"]["chi"]), "flags": int(flags),
+           "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
            "gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
            "frames": frames,
-           "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in frames])),
-           "seconds_per_frame": float(np.mean([fr["seconds"] for fr in frames])),
+           "newton_per_frame": float(np.mean([fr["newton_iters"] for fr in (conv or frames)])),
+           "seconds_per_frame": float(np.mean([fr["seconds"] for fr in (conv or frames)])),
            "frames_converged": len(conv), "max_newton": int(sc["params"]["max_newton"]),
-           "note": "newton_per_frame counts the Newton cap for frames that did not converge"}
+           "note": "newton_per_frame / seconds_per_frame: mean over the converged frames (over all frames, "
+                   "Newton cap included, when none converged)"}
     os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
