@@ -414,7 +414,8 @@ def run_ours(args):
     import glob
     npf_ref = None
     long_runs = {}
-    for rf in sorted(glob.glob(os.path.join(ROOT, "profiles", f"{args.config}_frames_r02*.json"))):
+    pat = "c4*" if args.config.startswith("c4") else args.config  # the C4 starts share the scene
+    for rf in sorted(glob.glob(os.path.join(ROOT, "profiles", f"{pat}_frames_r02*.json"))):
         with open(rf) as f:
             lr = json.load(f)
         tag = os.path.basename(rf)[:-5]

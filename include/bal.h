@@ -71,6 +71,12 @@ typedef struct { double E, nu, rho; } bal_material;
                                     * R-FRIC1 freeze (anchors frozen once min ||e|| has not halved in 10
                                     * Newton iterations) */
 
+#define BAL_CCD_LITERAL 64u  /* literal P:468 CCD activation d_TOC < eps + dhat instead of DESIGN.md R-CCD2's
+                              * eps + min(dhat, 1e-2 d_0) (ablation: shown to stall the line search) */
+#define BAL_PCG_LITERAL_STALL 128u /* literal P:757 / Q15 stagnation test on the residual norm (stop when the
+                                    * best ||r|| of the last window is no better than the best before it)
+                                    * instead of DESIGN.md R-PCG1's CG-objective test (ablation) */
+
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {
   double h;              /* time step (s) */
@@ -88,7 +94,8 @@ typedef struct {
   int32_t max_newton;    /* 1000 (Q13) */
   int32_t max_pcg;       /* 20000 (Q16) */
   int64_t max_constraints; /* constraint budget, P:440 (Q36) */
-  uint32_t flags;        /* BAL_NO_WARMSTART | BAL_NO_AUGLAG | BAL_FRICTION_LAGGED | BAL_SIGMA_CAP */
+  uint32_t flags;        /* BAL_NO_WARMSTART | BAL_NO_AUGLAG | BAL_FRICTION_LAGGED | BAL_SIGMA_CAP | BAL_SIGMA_MIN |
+                          * BAL_FRICTION_NO_FREEZE | BAL_CCD_LITERAL | BAL_PCG_LITERAL_STALL */
 } bal_params;
 
 /* Per-step statistics (Table 1 columns "avg. #iters (Newton)", "#cons"). */

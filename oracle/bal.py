@@ -38,6 +38,8 @@ FLAG_NO_AUGLAG = 2
 FLAG_SIGMA_CAP = 8  # NEXT-1: sigma ceiling 1e8 sigma0 (the GPU's BAL_SIGMA_CAP)
 FLAG_SIGMA_MIN = 16  # min(1.2 sigma, 100 sigma0) reading of Alg. 1 line 16 (the GPU's BAL_SIGMA_MIN)
 FLAG_FRICTION_NO_FREEZE = 32  # literal per-iteration anchors (disables R-FRIC1)
+FLAG_CCD_LITERAL = 64  # literal P:468 CCD activation eps + dhat (disables R-CCD2; the GPU's BAL_CCD_LITERAL)
+FLAG_PCG_LITERAL_STALL = 128  # literal residual stagnation test (Q15; disables R-PCG1; BAL_PCG_LITERAL_STALL)
 FREEZE_WINDOW = 10  # R-FRIC1 window (the GPU's kFreezeWindow)
 
 
@@ -306,7 +308,7 @@ class Oracle:
                 x0, ws_it = la.warm_start(A, b, asm["groups"], Dinv, m.fixed, float(p["ws_rel_tol"]),
                                           int(p["ws_max_iters"]))
             pst = la.pcg(A, b, x0, Dinv, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
-                         int(p["max_pcg"]))
+                         int(p["max_pcg"]), bool(self.flags & FLAG_PCG_LITERAL_STALL))
             resumes = 0
             while True:
                 dirn = pst.x.copy()
@@ -317,7 +319,8 @@ class Oracle:
                     safeguard = True
                 P = dirn.reshape(-1, 3)
                 cpt, cee = cm.candidates(m, x, x + P, dhat)
-                a_ccd = ccdm.step_toi(x, P, cpt, cee, dhat)
+                a_ccd = ccdm.step_toi(x, P, cpt, cee, dhat,
+                                      np.inf if self.flags & FLAG_CCD_LITERAL else 1e-2)
                 alpha = min(1.0, a_ccd)
                 L0, _n0, S0 = self.energy(x, st, cpt, cee)
                 halvings = 0

@@ -126,7 +126,7 @@ def _signed_dist(ftype, P):
     return float(np.dot(a0 - b0, np.cross(a1 - a0, b1 - b0)))
 
 
-def pair_toi(ftype, x, dx, ids, dhat):
+def pair_toi(ftype, x, dx, ids, dhat, d0frac=1e-2):
     """Conservative TOI of one PT or EE feature pair (role-ordered ids) moving by dx."""
     X0 = x[ids]
     DX = dx[ids]
@@ -141,7 +141,7 @@ def pair_toi(ftype, x, dx, ids, dhat):
         return min(1.0, 0.9 * d0 / (ma + mb))
     roots = cubic_roots(a, b, c, d)
     d0 = np.sqrt(resolve_features(x, ftype, ids[None])[0][0])
-    thr = EPS + min(dhat, 1e-2 * d0)  # R-CCD2: activation margin scaled by the current gap
+    thr = EPS + min(dhat, d0frac * d0)  # R-CCD2; d0frac = inf: P:468's literal eps + dhat
     t_prev = 0.0
     for t in roots:
         xt = x.copy()
@@ -167,12 +167,12 @@ def pair_toi(ftype, x, dx, ids, dhat):
     return 1.0
 
 
-def step_toi(x, dx, pt, ee, dhat):
+def step_toi(x, dx, pt, ee, dhat, d0frac=1e-2):
     """alpha_CCD = min over candidate pairs of the conservative TOI (1.0 if none)."""
     tmin = 1.0
     for ftype, pairs in ((PT, pt), (EE, ee)):
         for ids in pairs:
-            t = pair_toi(ftype, x, dx, ids, dhat)
+            t = pair_toi(ftype, x, dx, ids, dhat, d0frac)
             if t < tmin:
                 tmin = t
     return tmin

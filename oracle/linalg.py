@@ -59,7 +59,19 @@ def pcg_start(A, b, x0, Dinv):
                     float(np.linalg.norm(b)))
 
 
-def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
+def stalled(st, window, literal=False):
+    """App. B stagnation at iteration st.k.  R-PCG1 (default): the CG objective decreased by
+    no more than STALL_REL of its total decrease over the last `window` iterations.  literal (Q15, the
+    residual reading): the best ||r_j|| of the last window is no better than the best before it."""
+    k = st.k
+    if window <= 0 or k < window:
+        return False
+    if literal:
+        return min(st.hist[k - window + 1:k + 1]) >= min(st.hist[:k - window + 1])
+    return (st.dec[k] - st.dec[k - window]) <= STALL_REL * st.dec[k]
+
+
+def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters, literal_stall=False):
     """Run PCG iterations on st until a stop condition or until st.k reaches max_iters."""
     while True:
         rn = st.hist[-1]
@@ -70,7 +82,7 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
             st.stop = STOP_CONVERGED
             return st
         k = st.k
-        if k >= window and (st.dec[k] - st.dec[k - window]) <= STALL_REL * st.dec[k]:
+        if stalled(st, window, literal_stall):
             st.stop = STOP_STAGNATED
             return st
         if k >= max_iters:
@@ -78,7 +90,7 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters):
             return st
         q = A @ st.p
         pq = float(st.p @ q)
-        alpha = st.rz / pq
+        alpha = st.rz / pq if pq != 0.0 else np.nan  # as the GPU: 0/0 -> NaN -> NaN stop next check
         st.dec.append(st.dec[-1] + 0.5 * alpha * st.rz)  # phi(x + a p) = phi(x) - a rho / 2
         st.x = st.x + alpha * st.p
         st.r = st.r - alpha * q
@@ -101,9 +113,9 @@ def stop_margin(st, tol):
     return min(abs(h / ref - 1.0) for h in st.hist[-2:])
 
 
-def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000):
+def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False):
     st = pcg_start(A, b, x0, Dinv)
-    return pcg_run(A, Dinv, st, tol, window, max_iters)
+    return pcg_run(A, Dinv, st, tol, window, max_iters, literal_stall)
 
 
 class CGState(PCGState):
@@ -129,7 +141,7 @@ def cg_start(A, b, x0, Dinv):
     return st
 
 
-def cg_run(A, Dinv, st, tol, window, max_iters):
+def cg_run(A, Dinv, st, tol, window, max_iters, literal_stall=False):
     """Chronopoulos-Gear iterations on st until a stop condition or st.k reaches max_iters.  Stop
     rules and their order as pcg_run (App. B, Q14, R-PCG1), checked on ||r_k|| before step k."""
     while True:
@@ -141,7 +153,7 @@ def cg_run(A, Dinv, st, tol, window, max_iters):
         if rn <= tol * st.bnorm:
             st.stop = STOP_CONVERGED
             return st
-        if k >= window and (st.dec[k] - st.dec[k - window]) <= STALL_REL * st.dec[k]:
+        if stalled(st, window, literal_stall):
             st.stop = STOP_STAGNATED
             return st
         if k >= max_iters:
@@ -166,8 +178,8 @@ def cg_run(A, Dinv, st, tol, window, max_iters):
         st.z = st.u
 
 
-def pcg_cg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000):
-    return cg_run(A, Dinv, cg_start(A, b, x0, Dinv), tol, window, max_iters)
+def pcg_cg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False):
+    return cg_run(A, Dinv, cg_start(A, b, x0, Dinv), tol, window, max_iters, literal_stall)
 
 
 def warm_start(A, b, groups, Dinv, fixed, tol=1e-2, max_iters=100):

@@ -29,6 +29,8 @@ BAL_FRICTION_LAGGED = 4
 BAL_SIGMA_CAP = 8
 BAL_SIGMA_MIN = 16
 BAL_FRICTION_NO_FREEZE = 32
+BAL_CCD_LITERAL = 64
+BAL_PCG_LITERAL_STALL = 128
 
 
 class bal_mesh(C.Structure):

@@ -574,7 +574,8 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
       broad_phase(st, w.cw, w.cand_sw, c->V, c->sverts.ptr, c->F, c->tris.ptr, c->E, c->edges.ptr, w.x.ptr,
                   w.trial.ptr, dhat, c->fixed.ptr);
       mark("swept-bp", w.cand_sw.npt, w.cand_sw.nee);
-      a_ccd = ccd_step_toi(st, w.cw, w.cand_sw, w.x.ptr, w.dir.ptr, dhat);
+      a_ccd = ccd_step_toi(st, w.cw, w.cand_sw, w.x.ptr, w.dir.ptr, dhat,
+                           (c->prm.flags & BAL_CCD_LITERAL) ? INFINITY : 1e-2);
       mark("ccd");
       alpha = std::min(1.0, a_ccd);
       const Energy E0 = energy(c, w, w.x.ptr, w.cand_sw, sigma);

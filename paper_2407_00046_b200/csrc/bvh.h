@@ -51,7 +51,8 @@ int constraint_set(cudaStream_t st, ConstraintSet& cs, const Candidates& c, cons
 void barrier_energy(cudaStream_t st, CollisionWork& w, const ConstraintSet& cs, double sigma, double dhat,
                     double* out_sum, double* out_min);
 double ccd_step_toi(cudaStream_t st, CollisionWork& w, const Candidates& c, const double* x, const double* dx,
-                    double dhat);
+                    double dhat,
+                    double d0frac);
 void key_distances(cudaStream_t st, int n, const int* keys, const double* x, double* d);
 void phi_al_energy(cudaStream_t st, CollisionWork& w, int n, const double* d, const double* mu, const double* s,
                    double sigma, double dhat, double* out_sum, double* out_min, double* out_abs_sum);

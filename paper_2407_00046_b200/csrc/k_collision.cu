@@ -3,7 +3,7 @@
 //  * constraint_set: resolve every candidate feature pair at x (Q27), keep d < dhat,
 //    canonical 128-bit keys, radix sort + unique (Q28), distance recomputed from the key.
 //  * CCD: coplanarity cubic on [-eps, 1+eps], Newton-bisection on the monotone pieces
-//    split at the roots of c'(t), deflation (Q31), activation d_TOC < dhat + eps, conservative
+//    split at the roots of c'(t), deflation (Q31), activation d_TOC < eps + min(dhat, 1e-2 d_0) (R-CCD2; P:468's eps + dhat with BAL_CCD_LITERAL), conservative
 //    TOI with the reference-frame sign test and x0.9 backtracking (fig:ccd_toi; DESIGN R-CCD1).
 //  * energies: sigma * sum b(d; dhat) over C(x) and the A' terms mu (dhat + s - d) + sigma b(d; dhat + s)
 //    (eq:aug-lag); deterministic fixed-order reductions.
@@ -266,7 +266,7 @@ BAL_D double signed_dist(int ftype, const d3 P[4]) {
   return dot(P[0] - P[2], cross(P[1] - P[0], P[3] - P[2]));
 }
 
-BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat) {
+BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat, double d0frac) {
   const d3 e0[3] = {X0[1] - X0[0], X0[2] - X0[0], X0[3] - X0[0]};
   const d3 f[3] = {DX[1] - DX[0], DX[2] - DX[0], DX[3] - DX[0]};
   const double dd = det3(e0[0], e0[1], e0[2]);
@@ -288,9 +288,10 @@ BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat) {
   double roots[3];
   const int nr = cubic_roots(aa, bb, cc, dd, roots);
   if (nr == 0) return 1.0;
-  // DESIGN.md R-CCD2: activation margin eps + min(dhat, 1e-2 d_0) (P:468 writes eps + dhat)
+  // DESIGN.md R-CCD2: activation margin eps + min(dhat, 1e-2 d_0) (P:468 writes eps + dhat: the
+  // literal reading is d0frac = +inf, flag BAL_CCD_LITERAL)
   const double d0 = sqrt(resolve(ftype, X0[0], X0[1], X0[2], X0[3]).D);
-  const double thr = kCcdEps + fmin(dhat, 1e-2 * d0);
+  const double thr = kCcdEps + fmin(dhat, d0frac * d0);
   double t_prev = 0.0;
   for (int i = 0; i < nr; ++i) {
     const double t = roots[i];
@@ -328,7 +329,7 @@ BAL_D double pair_toi(int ftype, const d3 X0[4], const d3 DX[4], double dhat) {
 }
 
 __global__ void k_ccd(int n, int ftype, const int4* __restrict__ pairs, const double* __restrict__ x,
-                      const double* __restrict__ dx, double dhat, double* out) {
+                      const double* __restrict__ dx, double dhat, double d0frac, double* out) {
   __shared__ double sh[kRedThreads / 32];
   double tmin = 1.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -339,14 +340,14 @@ __global__ void k_ccd(int n, int ftype, const int4* __restrict__ pairs, const do
       X0[k] = ld3(x, id[k]);
       DX[k] = ld3(dx, id[k]);
     }
-    tmin = fmin(tmin, pair_toi(ftype, X0, DX, dhat));
+    tmin = fmin(tmin, pair_toi(ftype, X0, DX, dhat, d0frac));
   }
   tmin = block_min<kRedThreads>(tmin, sh);
   if (threadIdx.x == 0) out[blockIdx.x] = tmin;
 }
 
 double ccd_step_toi(cudaStream_t st, CollisionWork& w, const Candidates& c, const double* x, const double* dx,
-                    double dhat) {
+                    double dhat, double d0frac) {
   w.toi.reserve(2 * kRedBlocks + 2);
   w.part.reserve(kRedBlocks);
   const int nb = kRedBlocks;
@@ -354,8 +355,8 @@ double ccd_step_toi(cudaStream_t st, CollisionWork& w, const Candidates& c, cons
   // initialise both halves to 1.0 via a tiny fill of partials
   std::vector<double> ones(2 * nb, 1.0);
   CK(cudaMemcpyAsync(o, ones.data(), 2 * nb * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (c.npt) k_ccd<<<nb, kRedThreads, 0, st>>>(c.npt, T_PT, c.pt.ptr, x, dx, dhat, o);
-  if (c.nee) k_ccd<<<nb, kRedThreads, 0, st>>>(c.nee, T_EE, c.ee.ptr, x, dx, dhat, o + nb);
+  if (c.npt) k_ccd<<<nb, kRedThreads, 0, st>>>(c.npt, T_PT, c.pt.ptr, x, dx, dhat, d0frac, o);
+  if (c.nee) k_ccd<<<nb, kRedThreads, 0, st>>>(c.nee, T_EE, c.ee.ptr, x, dx, dhat, d0frac, o + nb);
   CK(cudaGetLastError());
   launch_min(st, 2 * nb, o, w.part.ptr, o + 2 * nb);
   double t = 1.0;

@@ -145,6 +145,8 @@ inline bool spmv_symmetric_enabled() { return spmv_mode() == 0; }
 struct PcgScal {
   double rz, pq, alpha, beta, rr, bnorm, tol, dec;
   int k, stop, done, max_iters, window, hcap;  // hist[0..hcap) = ||r_k||, hist[hcap..) = phi_0 - phi_k
+  int lit;      // BAL_PCG_LITERAL_STALL: Q15 residual-minimum stagnation test instead of R-PCG1
+  double pmin;  // literal test: min ||r_j|| over j <= k - window (maintained incrementally)
 };
 constexpr double kStallRel = 1e-10;  // DESIGN.md R-PCG1
 // warm-start per-group scalars

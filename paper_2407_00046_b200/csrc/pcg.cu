@@ -2,6 +2,7 @@
 // the App. B policy (Q14-Q16).  All scalars stay on the device; the host only polls
 // the device `done` flag once per batch of kBatch iterations (kernels early-exit once done).
 #include <climits>
+#include <cmath>
 #include <cstring>
 
 #include "ctx.h"
@@ -221,6 +222,8 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.window = window;
   h.max_iters = max_iters;
   h.hcap = hcap;
+  h.lit = (c->prm.flags & BAL_PCG_LITERAL_STALL) ? 1 : 0;
+  h.pmin = INFINITY;
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
   if (ts_usable(S)) {

@@ -15,6 +15,7 @@
 
 #include "ctx.h"
 #include "reduce.cuh"
+#include <cmath>
 
 namespace bal {
 
@@ -557,6 +558,8 @@ int pcg_solve_dist(bal_ctx* c, const double* rhs, const double* x0, double* x_ou
   h.window = window;
   h.max_iters = max_iters;
   h.hcap = hcap;
+  h.lit = (c->prm.flags & BAL_PCG_LITERAL_STALL) ? 1 : 0;
+  h.pmin = INFINITY;
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   tp_halo(c, c->px.ptr);
   launch_spmv(st, So, C, c->px.ptr, c->pq.ptr);

@@ -63,8 +63,17 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
   // its total decrease over the last W iterations
   const int W = sc->window;
   if (W > 0 && k >= W) {
-    const double* dh = hist + sc->hcap;
-    if (dh[k] - dh[k - W] <= kStallRel * dh[k]) {
+    bool stall;
+    if (sc->lit) {  // literal P:757 / Q15: the best residual of the last W iterations is no better
+      sc->pmin = fmin(sc->pmin, hist[k - W]);  // than the best before them
+      double wmin = rn;
+      for (int j = k - W + 1; j < k; ++j) wmin = fmin(wmin, hist[j]);
+      stall = wmin >= sc->pmin;
+    } else {  // R-PCG1
+      const double* dh = hist + sc->hcap;
+      stall = dh[k] - dh[k - W] <= kStallRel * dh[k];
+    }
+    if (stall) {
       sc->stop = 1;
       sc->done = 1;
       return;

@@ -145,3 +145,91 @@ def test_bal_equals_plain_barrier_newton_fixed_point():
     x1, _, s1 = o1.step(sc["x0"], sc["v0"])
     x2, _, s2 = o2.step(sc["x0"], sc["v0"])
     assert np.linalg.norm(x1 - x2) <= 1e-6 * np.linalg.norm(x1 - sc["x0"]) + 1e-9
+
+
+# ---------------------------------------------------------------- lumped mass
+def test_lumped_mass_pins():
+    """m_j = sum over the tets at j of rho V_e / 4: one tet of edge 0.1 m (V = 1e-3 / 6 m^3, by hand)
+    gives rho V / 4 per node; the two C1 cubes (edge 1.0 m each, so total volume 2 m^3 from the scene
+    recipe, not from the tets) give sum m = 2 rho; masses are positive."""
+    from oracle.mesh import precompute
+    sc = scenes.make_single_tet(0)
+    m = precompute(sc)
+    free = ~m.fixed
+    np.testing.assert_allclose(m.mass[free], 1e3 * (1e-3 / 6.0) / 4.0, rtol=1e-12)
+    c = scenes.make_cubes(1)
+    mc = precompute(c)
+    assert np.sum(mc.mass) == pytest.approx(2.0 * 1e3, rel=1e-12)
+    assert np.all(mc.mass[~mc.fixed] > 0)
+
+
+# ---------------------------------------------------------------- sigma^0 (P:285-289, Q7)
+def test_sigma0_through_assembly_and_floor():
+    """Oracle.sigma0 end to end: with the inertial predictor chosen so that the non-barrier gradient
+    is g_E = -K g_b (y = x + h^2 M^-1 (grad Psi + K g_b)), the least-squares penalty is exactly K
+    (Q7) whenever K exceeds the floor; with no active constraint sigma^0 is the floor m_bar / h^2."""
+    from oracle.energy import nh_stencils
+    sc = scenes.make_single_tet(3, height=0.0004)  # within dhat of the plane
+    o = Oracle(sc)
+    m = o.mesh
+    x = sc["x0"].copy()
+    pt, ee = cm.candidates(m, x, x, o.dhat)
+    keys, _d = cm.constraint_set(x, pt, ee, o.dhat)
+    assert len(keys) > 0
+    N = o.N
+    gb = np.zeros((N, 3))
+    for ids, g, _H, _dd, _dp in cm.contact_stencils(x, keys, np.ones(len(keys)), np.zeros(len(keys)),
+                                                    np.zeros(len(keys)), np.zeros(len(keys)), 1.0, o.dhat):
+        gb[ids] += g.reshape(-1, 3)
+    gpsi = np.zeros((N, 3))
+    _v, g, _H = nh_stencils(x, m)
+    for k in range(4):
+        np.add.at(gpsi, m.tets[:, k], g[:, 3 * k:3 * k + 3])
+    floor = float(np.mean(m.mass[~m.fixed])) / o.h ** 2
+    K = 10.0 * floor
+    y = x.copy()
+    free = ~m.fixed
+    y[free] = x[free] + o.h ** 2 * (gpsi[free] + K * gb[free]) / m.mass[free, None]
+    st = dict(y=y, x_t=x, ap_keys=np.zeros((0, 5), np.int64), ap_mu=np.zeros(0), ap_s=np.zeros(0), fr_keys=None)
+    assert o.sigma0(x, st, keys) == pytest.approx(K, rel=1e-9)
+    assert o.sigma0(x, st, np.zeros((0, 5), np.int64)) == pytest.approx(floor, rel=1e-15)
+
+
+# ---------------------------------------------------------------- literal readings (DESIGN.md §3)
+def test_literal_ccd_activation_stalls_the_line_search():
+    """P:468's literal activation d_TOC < eps + dhat (flag, R-CCD2 off): on C1 a pair already within
+    dhat that slides past a neighbouring primitive's plane is truncated every Newton iteration;
+    alpha_CCD shrinks ~10x per iteration until the App. B resumes give up (the reason for R-CCD2)."""
+    from oracle.bal import FLAG_CCD_LITERAL, NotConverged
+    sc = scenes.make_cubes(1)
+    sc["params"]["max_pcg"] = 400  # the App. B resumes give up sooner (the stall is the same)
+    o = Oracle(sc, flags=FLAG_CCD_LITERAL)
+    x, v = sc["x0"], sc["v0"]
+    tr = []
+    with pytest.raises(NotConverged):
+        for _ in range(3):
+            tr = []
+            x, v, _s = o.step(x, v, tr)
+    a = [t["alpha_ccd"] for t in tr][-4:]
+    assert all(0.05 < a[i + 1] / a[i] < 0.2 for i in range(len(a) - 1)), a
+
+
+def test_literal_residual_stagnation_stops_with_a_useless_direction():
+    """Q15's literal residual-minimum test (flag, R-PCG1 off) on an ill-conditioned SPD system whose CG
+    residual norm oscillates: it stops after one window with ||r|| above ||b|| (CG never improved on
+    x0 = 0 in the residual norm), although the CG objective was still decreasing (the reason for
+    R-PCG1's objective-based test)."""
+    import scipy.sparse as sp
+    from oracle import linalg as la
+    rng = np.random.default_rng(0)
+    n = 600
+    A = sp.diags(np.logspace(0, 9, n)).tocsr()
+    b = rng.normal(size=n)
+    Dinv = np.tile(np.eye(3), (n // 3, 1, 1))
+    lit = la.pcg(A, b, np.zeros(n), Dinv, tol=1e-4, window=100, max_iters=2000, literal_stall=True)
+    assert lit.stop == la.STOP_STAGNATED and lit.k == 100
+    assert lit.hist[-1] > lit.bnorm
+    obj = la.pcg(A, b, np.zeros(n), Dinv, tol=1e-4, window=100, max_iters=2000)
+    assert obj.stop == la.STOP_CAP  # the objective kept decreasing: no stagnation stop
+    phi = lambda x: 0.5 * x @ (A @ x) - b @ x  # noqa: E731
+    assert phi(obj.x) < phi(lit.x) < 0.0
