@@ -239,6 +239,10 @@ typedef struct {
 bal_status bal_assemble(bal_ctx* ctx, const double* x, const bal_contact_state* cs,
                         bal_system_view* out_view);
 
+/* Views of the system the last Newton iteration (bal_step / bal_frame_iterate) or bal_assemble
+ * assembled (same fields and validity as bal_assemble's out_view).  Errors: BAL_E_INVALID_ARG. */
+bal_status bal_get_system(bal_ctx* ctx, bal_system_view* out_view);
+
 /* y = A v on the last assembled (or loaded) system.  v, y: device [3N]. */
 bal_status bal_spmv(bal_ctx* ctx, const double* v, double* y);
 

@@ -19,7 +19,7 @@ from ._lib import (BAL_CCD_LITERAL, BAL_FRICTION_LAGGED, BAL_FRICTION_NO_FREEZE,
 
 __all__ = ["BalError", "BalCtx", "bal_init", "bal_step", "bal_step_host", "bal_assemble", "bal_spmv", "bal_pcg",
            "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "bal_nccl_unique_id", "bal_dist_info", "bal_spmv_rows",
-           "bal_halo_plan", "bal_halo_pack", "bal_halo_unpack", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG",
+           "bal_halo_plan", "bal_halo_pack", "bal_halo_unpack", "bal_get_system", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG",
            "BAL_FRICTION_LAGGED", "BAL_SIGMA_CAP", "BAL_SIGMA_MIN", "BAL_FRICTION_NO_FREEZE", "BAL_CCD_LITERAL",
            "BAL_PCG_LITERAL_STALL", "lib_path"]
 
@@ -315,14 +315,26 @@ def bal_assemble(ctx, x, active_keys=(), aprime_keys=(), aprime_mu=(), aprime_s=
         cs.y = _lib.ptr(yy, C.c_double)
     v = bal_system_view()
     _check(ctx, _lib.lib.bal_assemble(ctx.handle, *_vecs(ctx, x), C.byref(cs), C.byref(v)))
+    return _views(v, x.device)
+
+
+def bal_get_system(ctx, device=None):
+    """Views of the system the last Newton iteration or bal_assemble assembled (copies, dict of
+    torch tensors as bal_assemble returns)."""
+    v = bal_system_view()
+    _check(ctx, _lib.lib.bal_get_system(ctx.handle, C.byref(v)))
+    return _views(v, device or torch.device(f"cuda:{ctx.device}"))
+
+
+def _views(v, device):
     N = v.n_nodes
 
     def view(p, n, dtype):
         if not p or n == 0:
-            return torch.zeros(0, dtype=dtype, device=x.device)
-        return _wrap(p, n, dtype, x.device).clone()
+            return torch.zeros(0, dtype=dtype, device=device)
+        return _wrap(p, n, dtype, device).clone()
 
-    out = dict(
+    return dict(
         n_nodes=N,
         static_row_ptr=view(v.static_row_ptr, N + 1, torch.int32),
         static_col=view(v.static_col, v.nnzb_static, torch.int32),
@@ -340,7 +352,6 @@ def bal_assemble(ctx, x, active_keys=(), aprime_keys=(), aprime_mu=(), aprime_s=
         contact_lbar=view(v.contact_lbar, v.n_contact_stencils, torch.float64),
         contact_stencil_nodes=view(v.contact_stencil_nodes, 4 * v.n_contact_stencils, torch.int32),
     )
-    return out
 
 
 class _CAI:

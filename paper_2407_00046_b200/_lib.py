@@ -120,6 +120,7 @@ _sig = {
     "bal_frame_finish": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_frame_peek": (C.c_int, [C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(bal_contact_state), C.POINTER(bal_system_view)]),
+    "bal_get_system": (C.c_int, [C.c_void_p, C.POINTER(bal_system_view)]),
     "bal_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bal_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_pcg_opts),
                           C.POINTER(bal_pcg_stats)]),

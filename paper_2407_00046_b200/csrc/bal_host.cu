@@ -42,6 +42,7 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   pin_ptr.upload(H.pin_ptr.data(), H.pin_ptr.size(), st);
   meta.upload(H.meta.data(), std::max<size_t>(H.meta.size(), 16), st);
   part.reserve(3 * (size_t)std::max(H.nslots, 1));
+  crange.reserve(std::max(H.ntiles, 1));
   plan = TsPlan();
   plan.n = N;
   plan.ntiles = H.ntiles;
@@ -49,9 +50,13 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   plan.desc = desc.ptr;
   plan.cap_rows = H.cap_rows;
   plan.o_crp = H.o_crp;
+  plan.o_ccv = H.o_ccv;
+  plan.o_ccol = H.o_ccol;
+  plan.o_cvv = H.o_cvv;
   plan.meta = meta.ptr;
   plan.pin_ptr = pin_ptr.ptr;
   plan.part = part.ptr;
+  plan.crange = crange.ptr;
   plan.o_meta = H.o_meta;
   plan.o_val = H.o_val;
   plan.o_vt = H.o_vt;
@@ -494,6 +499,7 @@ void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
                 c->sp_sym ? c->lval.ptr : nullptr);
   build_contact_pattern(st, c->cw, ns, c->nodes_c.ptr, c->fixed.ptr, N, c->stage_c.ptr);
   if (ns == 0) c->cw.nslots = 0;
+  if (c->sp_ts.ready && c->cw.nslots > 0) launch_ts_crange(st, c->sp_ts.plan, c->cw.row_ptr.ptr);
   node_finalize(st, N, x, y, c->mass.ptr, inv_h2, c->fixed.ptr, c->sp, c->grad_e.ptr, c->lbar_e.ptr, c->sval.ptr,
                 &c->cw, c->grad_c.ptr, c->lbar_c.ptr, c->grad.ptr, c->e_node.ptr, c->group.ptr, c->dinv.ptr);
   c->launches += 6;
@@ -504,6 +510,30 @@ void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
 
 // ================================================================== C ABI
 static thread_local std::string g_init_err;
+
+static void fill_view(const bal_ctx* c, bal_system_view* v) {
+  std::memset(v, 0, sizeof(*v));
+  v->n_nodes = c->N;
+  v->nnzb_static = c->sp.nnzb;
+  v->static_row_ptr = c->sp.row_ptr;
+  v->static_col = c->sp.col;
+  v->static_val = c->sval.ptr;
+  v->nnzb_contact = c->cw.nslots;
+  v->contact_row_ptr = c->cw.nslots ? c->cw.row_ptr.ptr : nullptr;
+  v->contact_col = c->cw.nslots ? c->cw.col.ptr : nullptr;
+  v->contact_val = c->cw.nslots ? c->cw.val.ptr : nullptr;
+  v->diag_inv = c->dinv.ptr;
+  v->grad = c->grad.ptr;
+  v->e_node = c->e_node.ptr;
+  v->group = c->group.ptr;
+  v->n_elastic = c->T;
+  v->elastic_blocks = c->stage_e.ptr;
+  v->elastic_lbar = c->lbar_e.ptr;
+  v->n_contact_stencils = c->n_contact + c->n_fric;
+  v->contact_blocks = c->stage_c.ptr;
+  v->contact_lbar = c->lbar_c.ptr;
+  v->contact_stencil_nodes = c->nodes_c.ptr;
+}
 
 extern "C" {
 
@@ -582,29 +612,16 @@ bal_status bal_assemble(bal_ctx* c, const double* x, const bal_contact_state* cs
     }
     run_assembly(c, x, c->y.ptr, cs->sigma);
     CK(cudaStreamSynchronize(st));
-    if (v) {
-      std::memset(v, 0, sizeof(*v));
-      v->n_nodes = N;
-      v->nnzb_static = c->sp.nnzb;
-      v->static_row_ptr = c->sp.row_ptr;
-      v->static_col = c->sp.col;
-      v->static_val = c->sval.ptr;
-      v->nnzb_contact = c->cw.nslots;
-      v->contact_row_ptr = c->cw.nslots ? c->cw.row_ptr.ptr : nullptr;
-      v->contact_col = c->cw.nslots ? c->cw.col.ptr : nullptr;
-      v->contact_val = c->cw.nslots ? c->cw.val.ptr : nullptr;
-      v->diag_inv = c->dinv.ptr;
-      v->grad = c->grad.ptr;
-      v->e_node = c->e_node.ptr;
-      v->group = c->group.ptr;
-      v->n_elastic = c->T;
-      v->elastic_blocks = c->stage_e.ptr;
-      v->elastic_lbar = c->lbar_e.ptr;
-      v->n_contact_stencils = c->n_contact + c->n_fric;
-      v->contact_blocks = c->stage_c.ptr;
-      v->contact_lbar = c->lbar_c.ptr;
-      v->contact_stencil_nodes = c->nodes_c.ptr;
-    }
+    if (v) fill_view(c, v);
+    return BAL_OK;
+  });
+}
+
+bal_status bal_get_system(bal_ctx* c, bal_system_view* v) {
+  if (!c || !v) return BAL_E_INVALID_ARG;
+  return guard(c, [&]() {
+    CK(cudaStreamSynchronize(c->st));
+    fill_view(c, v);
     return BAL_OK;
   });
 }

@@ -217,3 +217,52 @@ def test_c4_contact_stencils_and_spmv_with_contacts(c4_contact):
     yg = torch.empty(3 * N, dtype=torch.float64, device=DEV)
     bal.bal_spmv(ctx, _t(v), yg)
     assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)
+
+
+# --------------------------------------------------------------------------- contact-rich C4 start
+@pytest.fixture(scope="module")
+def c4_settled():
+    """The bench workload: C4's contact-rich start (scenes.make_puffer_net(settled=True)), after one
+    inexact-Newton iteration of its first frame (the library's own constraint set, ~2.5e5 pairs)."""
+    sc = scenes.make_puffer_net(seed=4, settled=True)
+    ctx = bal.bal_init(sc)
+    x = torch.as_tensor(sc["x0"].ravel(), device=DEV)
+    v = torch.as_tensor(sc["v0"].ravel(), device=DEV)
+    bal.bal_frame_begin(ctx, x, v)
+    bal.bal_frame_iterate(ctx, 1)
+    out = bal.bal_get_system(ctx)
+    return sc, ctx, out
+
+
+def test_c4_settled_spmv_every_row_with_paper_scale_contacts(c4_settled):
+    """SpMV over every row of the static + contact system at paper-scale contact load (228K
+    avg / 292K max constraints) in the bench's launch configuration: element-wise 1e-12 of |A||v|
+    against the CSR product of the assembled blocks, bitwise repeatable."""
+    sc, ctx, out = c4_settled
+    assert bal.bal_get_trace(ctx, max_records=8)[-1]["nA"] > 2e5
+    N = len(sc["x0"])
+    A = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
+    assert out["contact_col"].numel() > 5e5
+    A = A + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
+    v = np.random.default_rng(6).normal(size=3 * N)
+    yg = torch.empty(3 * N, dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)
+    y2 = torch.empty_like(yg)
+    bal.bal_spmv(ctx, _t(v), y2)
+    assert torch.equal(yg, y2)
+
+
+def test_c4_settled_pcg_iterates(c4_settled):
+    """20 single-reduction PCG iterations on the contact-rich system vs the oracle's pcg_cg (1e-10)."""
+    sc, ctx, out = c4_settled
+    N = len(sc["x0"])
+    A = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
+    A = A + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
+    b = -_np(out["grad"])
+    Dinv = dinv_full(_np(out["diag_inv"]))
+    xg = torch.empty(3 * N, dtype=torch.float64, device=DEV)
+    s = bal.bal_pcg(ctx, _t(b), _t(np.zeros_like(b)), xg, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=20)
+    st = la.pcg_cg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=20)
+    assert s["iters"] == 20 == st.k
+    assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
