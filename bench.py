@@ -122,16 +122,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def job_throughput(local_seconds, units_per_rank, world, device):
+def job_throughput(local_seconds, units_per_rank, world, device, shared=False):
     """Max of the ranks' timed-region seconds (the job time) and the whole-job throughput
-    (units processed by all ranks / job time).  One all_reduce(MAX) when world > 1."""
+    (units processed by all ranks / job time).  One all_reduce(MAX) when world > 1.  shared: the
+    ranks cooperate on ONE problem (partitioned solve), so the job's units are one rank's count."""
     import torch
     import torch.distributed as dist
     t = torch.tensor([float(local_seconds)], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     s = float(t.item())
-    return s, world * units_per_rank / s
+    return s, (1 if shared else world) * units_per_rank / s
 
 
 def measured_peaks():
@@ -297,7 +298,17 @@ def run_ours(args):
     import paper_2407_00046_b200 as bal
 
     sc, wl = make_scene(args.config)
-    ctx = bal.bal_init(sc, device=local)
+    # N > 1: the partitioned solve of SURVEY §8(e) (vertex-domain row ranges, NCCL halo of p before
+    # every SpMV + one all-reduce per PCG iteration; strong scaling of the one C4 problem).
+    # BAL_BENCH_REPLICAS=1: N independent replicas instead (weak scaling, no data-path collective).
+    replicas = world > 1 and os.environ.get("BAL_BENCH_REPLICAS") == "1"
+    shared = world > 1 and not replicas
+    if shared:
+        obj = [bal.bal_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = bal.bal_init(sc, device=local, rank=rank, world=world, nccl_id=obj[0])
+    else:
+        ctx = bal.bal_init(sc, device=local)
     stream = torch.cuda.current_stream(dev)
     bal.bal_set_stream(ctx, stream)
     x = torch.as_tensor(sc["x0"].ravel(), device=dev)
@@ -333,7 +344,7 @@ def run_ours(args):
     d = {k: tot1[k] - tot0[k] for k in tot1 if k != "max_constraints"}
     pcg = d["pcg_iters"]
     newton = d["newton_iters"]
-    s_max, pcg_per_s = job_throughput(ms / 1000.0, pcg, world, dev)
+    s_max, pcg_per_s = job_throughput(ms / 1000.0, pcg, world, dev, shared)
     ms_max = 1000.0 * s_max
     new_frames = run.frames[nf0:]
     # SpMV roofline from the library's CUDA events around every SpMV launch in the timed region
@@ -379,7 +390,12 @@ def run_ours(args):
         E2E_NEWTON = 2
         prm = dict(sc["params"])
         prm["max_newton"] = E2E_NEWTON
-        ctx2 = bal.bal_init(sc, device=local, params=prm)
+        if shared:
+            obj = [bal.bal_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx2 = bal.bal_init(sc, device=local, params=prm, rank=rank, world=world, nccl_id=obj[0])
+        else:
+            ctx2 = bal.bal_init(sc, device=local, params=prm)
         xh = run.x.detach().cpu().numpy().copy()
         vh = run.v.detach().cpu().numpy().copy()
         torch.cuda.synchronize()
@@ -388,7 +404,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         _xn, _vn, st2 = bal.bal_step_host(ctx2, xh, vh, allow_unconverged=True)
         el = time.perf_counter() - t0
-        _s, e2e_v = job_throughput(el, st2["pcg_iters"], world, dev)
+        _s, e2e_v = job_throughput(el, st2["pcg_iters"], world, dev, shared)
         nb = 3 * 8 * len(sc["rest_x"])
         e2e = {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
                "newton_iters": st2["newton_iters"], "pcg_iters": st2["pcg_iters"], "seconds": el,
@@ -426,12 +442,14 @@ def run_ours(args):
             npf_ref = lr.get("newton_per_frame")
     line = {
         "metric": METRIC, "value": pcg_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong" if shared else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
                    "step": "one inexact-Newton iteration of Alg. 1 (constraint sets, stencils, assembly, warm "
                            "start, PCG, CCD line search, AL updates); frames continue across steps",
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"partitioned{world} (NCCL halo + allreduce)" if shared else
+                                   f"replicas{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (system ~0.5 GB/PCG iteration)"},
         "headline": {"ms_per_newton": ms_newton,
                      "active_constraints": {"avg": float(np.mean(nA_t)) if nA_t else None,
