@@ -247,7 +247,8 @@ bal_status bal_get_system(bal_ctx* ctx, bal_system_view* out_view);
 bal_status bal_spmv(bal_ctx* ctx, const double* v, double* y);
 
 typedef struct {
-  int32_t warm_start;   /* 1 = stiffness-grouped block-Jacobi warm start (Q20) */
+  int32_t warm_start;   /* 1 = stiffness-grouped block-Jacobi warm start (Q20), kept only if
+                         * phi(x0) = x0'Ax0/2 - b'x0 < 0 = phi(0) (DESIGN.md R-WS1; else x0 = 0) */
   double rel_tol;       /* ||r|| <= rel_tol ||b|| (App. B, Q14) */
   int32_t stall_window; /* App. B stagnation window (Q15); <= 0 disables */
   int32_t max_iters;
@@ -283,6 +284,9 @@ bal_status bal_load_bsr(bal_ctx* ctx, const bal_bsr_host* bsr);
 /* Residual history ||r_k||, k = 0..iters, of the last global PCG solve (HOST out[max_n]);
  * returns the number of entries written (or a negative bal_status). */
 int32_t bal_pcg_history(bal_ctx* ctx, double* out, int32_t max_n);
+/* Decrease of the CG objective phi_0 - phi_k, k = 0..iters, of the last global PCG solve (R-PCG1's
+ * stagnation measure; HOST out[max_n]); returns the number of entries written or a bal_status. */
+int32_t bal_pcg_objective_history(bal_ctx* ctx, double* out, int32_t max_n);
 
 /* Timing helper for the benchmark: run `iters` SpMV launches on the current system with CUDA
  * events on the ctx stream; returns the mean launch duration in microseconds. */

@@ -307,6 +307,10 @@ class Oracle:
             else:
                 x0, ws_it = la.warm_start(A, b, asm["groups"], Dinv, m.fixed, float(p["ws_rel_tol"]),
                                           int(p["ws_max_iters"]))
+                # DESIGN.md R-WS1: keep the warm start only if it is closer to the solution than 0 in
+                # the A-norm, i.e. phi(x0) = x0'A x0 / 2 - b'x0 < phi(0) = 0
+                if not (0.5 * float(x0 @ (A @ x0)) - float(b @ x0) < 0.0):
+                    x0 = np.zeros_like(b)
             pst = la.pcg(A, b, x0, Dinv, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
                          int(p["max_pcg"]), bool(self.flags & FLAG_PCG_LITERAL_STALL))
             resumes = 0

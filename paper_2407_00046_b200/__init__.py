@@ -259,6 +259,15 @@ def bal_get_trace(ctx, max_records=100000):
     return [dict(zip(TRACE_FIELDS, r.tolist())) for r in rows]
 
 
+def bal_pcg_objective_history(ctx, max_n=200000):
+    """phi_0 - phi_k (CG objective decrease), k = 0..iters, of the last global PCG solve."""
+    out = np.zeros(max_n)
+    n = _lib.lib.bal_pcg_objective_history(ctx.handle, _lib.ptr(out, C.c_double), max_n)
+    if n < 0:
+        raise BalError(n, "bal_pcg_objective_history")
+    return out[:n].copy()
+
+
 def bal_pcg_history(ctx, max_n=200000):
     """||r_k|| of the last global PCG solve, k = 0..iters."""
     out = np.zeros(max_n)

@@ -129,6 +129,7 @@ _sig = {
     "bal_get_trace": (C.c_int32, [C.c_void_p, c_double_p, C.c_int32]),
     "bal_spmv_counters": (C.c_int, [C.c_void_p, c_double_p]),
     "bal_pcg_history": (C.c_int32, [C.c_void_p, c_double_p, C.c_int32]),
+    "bal_pcg_objective_history": (C.c_int32, [C.c_void_p, c_double_p, C.c_int32]),
     "bal_kernel_launches": (C.c_int64, [C.c_void_p]),
     "bal_partition_rows": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, c_int_p]),
     "bal_ghost_columns": (C.c_int32, [C.c_int32, c_int_p, c_int_p, C.c_int32, C.c_int32, c_int_p, C.c_int32]),

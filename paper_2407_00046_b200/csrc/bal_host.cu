@@ -782,6 +782,15 @@ int32_t bal_pcg_history(bal_ctx* c, double* out, int32_t max_n) {
   return n;
 }
 
+int32_t bal_pcg_objective_history(bal_ctx* c, double* out, int32_t max_n) {
+  if (!c || !out || max_n <= 0) return BAL_E_INVALID_ARG;
+  const int n = std::min(max_n, c->h_scal ? c->h_scal->k + 1 : 0);
+  if (n <= 0) return 0;
+  if (cudaMemcpy(out, c->hist.ptr + c->h_scal->hcap, sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return BAL_E_CUDA;
+  return n;
+}
+
 bal_status bal_spmv_counters(const bal_ctx* c, double* out) {
   if (!c || !out) return BAL_E_INVALID_ARG;
   out[0] = c->spmv_ms;

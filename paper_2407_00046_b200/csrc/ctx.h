@@ -104,6 +104,7 @@ struct bal_ctx {
   bal::DevBuf<bal::GrpScal> gscal;
   bal::PcgScal* h_scal = nullptr;  // pinned
   int ngroups = 0;
+  bool ws_rejected = false;  // R-WS1: the last solve discarded its warm start
   // scratch
   bal::DevBuf<double> tmp_a, tmp_b, red;
   bal::DevBuf<int> tmp_i;

@@ -157,6 +157,23 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
   }
 }
 
+// phi(x0) = x0'(A x0)/2 - b'x0 = -x0'(b + r0)/2 with r0 = b - A x0 (pr after the init): true when the
+// warm start is not below phi(0) = 0 (R-WS1).  Two deterministic dot products and one host sync.
+static bool ws_guard_rejects(bal_ctx* c, const double* rhs) {
+  cudaStream_t st = c->st;
+  const int n3 = 3 * c->N;
+  c->red.reserve(kRedBlocks + 16);
+  double* out = c->red.ptr + kRedBlocks;
+  launch_dot(st, n3, c->px.ptr, rhs, c->red.ptr, out);
+  launch_dot(st, n3, c->px.ptr, c->pr.ptr, c->red.ptr, out + 1);
+  c->launches += 4;
+  double h[2];
+  CK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double phi = -0.5 * (h[0] + h[1]);
+  return !(phi < 0.0);
+}
+
 int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bool warm, double tol, int window,
               int max_iters, double ws_tol, int ws_max, bal_pcg_stats* stats) {
   if (c->dist.active)
@@ -165,6 +182,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   const int N = c->N;
   const Bsr S = c->static_bsr(), C = c->contact_bsr();
   if (stats) std::memset(stats, 0, sizeof(*stats));
+  c->ws_rejected = false;
   // hist[0, hcap): ||r_k||; hist[hcap, 2 hcap): cumulative CG objective decrease (R-PCG1).  Sized for
   // App. B resumes up to the max_pcg cap as well.
   const int hcap = std::max(max_iters, c->prm.max_pcg) + 8;
@@ -230,6 +248,16 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
     // single-reduction (Chronopoulos-Gear) PCG: init, then SpMV 0 (w_0 = A u_0, stop test at k = 0)
     launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
                    c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+    if (warm && ws_guard_rejects(c, rhs)) {
+      // DESIGN.md R-WS1: the warm start is used only when it is closer to the solution than x = 0 in the
+      // A-norm, phi(x0) = x0'A x0 / 2 - b'x0 < phi(0) = 0; else the solve starts from 0
+      CK(cudaMemsetAsync(c->px.ptr, 0, 3 * (size_t)N * sizeof(double), st));
+      CK(cudaMemsetAsync(c->pq.ptr, 0, 3 * (size_t)N * sizeof(double), st));
+      launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
+                     c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+      c->launches += 1;
+      c->ws_rejected = true;
+    }
     launch_spmv_ts_dot(st, S, C, c->pz.ptr, c->pq.ptr, S.ts->part, c->dpart.ptr, c->counter.ptr, c->scal.ptr,
                        c->upart.ptr, c->hist.ptr);
     c->launches += 3 + (S.ts ? 1 : 0);

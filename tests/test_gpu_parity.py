@@ -237,6 +237,8 @@ def test_warm_start_parity(cubes_state):
     s = bal.bal_pcg(ctx, _t(b), None, xg, warm_start=1, max_iters=0)
     x0, its = la.warm_start(A, b, asm["groups"], Dinv, o.mesh.fixed, 1e-2, 100)
     assert s["ws_iters_max"] == max(its.values())
+    phi0 = 0.5 * x0 @ (A @ x0) - b @ x0
+    assert phi0 < 0.0  # R-WS1 keeps it (phi(x0) < phi(0))
     assert np.linalg.norm(_np(xg) - x0) <= 1e-10 * np.linalg.norm(x0)
     # and the full warm-started solve reaches the App. B tolerance
     s = bal.bal_pcg(ctx, _t(b), None, xg, warm_start=1)
