@@ -330,12 +330,14 @@ def bal_assemble(ctx, x, active_keys=(), aprime_keys=(), aprime_mu=(), aprime_s=
 def bal_get_system(ctx, device=None):
     """Views of the system the last Newton iteration or bal_assemble assembled (copies, dict of
     torch tensors as bal_assemble returns)."""
+    import torch
     v = bal_system_view()
     _check(ctx, _lib.lib.bal_get_system(ctx.handle, C.byref(v)))
     return _views(v, device or torch.device(f"cuda:{ctx.device}"))
 
 
 def _views(v, device):
+    import torch
     N = v.n_nodes
 
     def view(p, n, dtype):

@@ -42,7 +42,6 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   pin_ptr.upload(H.pin_ptr.data(), H.pin_ptr.size(), st);
   meta.upload(H.meta.data(), std::max<size_t>(H.meta.size(), 16), st);
   part.reserve(3 * (size_t)std::max(H.nslots, 1));
-  crange.reserve(std::max(H.ntiles, 1));
   plan = TsPlan();
   plan.n = N;
   plan.ntiles = H.ntiles;
@@ -50,13 +49,9 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   plan.desc = desc.ptr;
   plan.cap_rows = H.cap_rows;
   plan.o_crp = H.o_crp;
-  plan.o_ccv = H.o_ccv;
-  plan.o_ccol = H.o_ccol;
-  plan.o_cvv = H.o_cvv;
   plan.meta = meta.ptr;
   plan.pin_ptr = pin_ptr.ptr;
   plan.part = part.ptr;
-  plan.crange = crange.ptr;
   plan.o_meta = H.o_meta;
   plan.o_val = H.o_val;
   plan.o_vt = H.o_vt;
@@ -499,7 +494,6 @@ void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
                 c->sp_sym ? c->lval.ptr : nullptr);
   build_contact_pattern(st, c->cw, ns, c->nodes_c.ptr, c->fixed.ptr, N, c->stage_c.ptr);
   if (ns == 0) c->cw.nslots = 0;
-  if (c->sp_ts.ready && c->cw.nslots > 0) launch_ts_crange(st, c->sp_ts.plan, c->cw.row_ptr.ptr);
   node_finalize(st, N, x, y, c->mass.ptr, inv_h2, c->fixed.ptr, c->sp, c->grad_e.ptr, c->lbar_e.ptr, c->sval.ptr,
                 &c->cw, c->grad_c.ptr, c->lbar_c.ptr, c->grad.ptr, c->e_node.ptr, c->group.ptr, c->dinv.ptr);
   c->launches += 6;

@@ -15,7 +15,6 @@ struct TsDev {
   bal::DevBuf<int4> desc;
   bal::DevBuf<unsigned char> meta;
   bal::DevBuf<double> part;
-  bal::DevBuf<int2> crange;
   bal::TsPlan plan;
   bool ready = false;
   // lower CSR (lrow[N+1], lcol) -> plan on the device; ready = false when the kernel cannot be used

@@ -256,11 +256,7 @@ bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol,
   P.o_vt = P.o_val + up128((size_t)P.cap_nb * 72 + 32);
   P.o_xv = P.o_vt + up128((size_t)P.cap_rows * 24 + 32);
   P.o_crp = P.o_xv + up128((size_t)std::max(P.cap_x, 1) * 24);
-  // contact blocks of the tile's rows (first kTsContactCap of its range): values, columns, v there
-  P.o_ccv = P.o_crp + up128((size_t)(P.cap_rows + 1) * 4);
-  P.o_ccol = P.o_ccv + up128((size_t)kTsContactCap * 72 + 32);
-  P.o_cvv = P.o_ccol + up128((size_t)kTsContactCap * 4 + 32);
-  P.stage_bytes = P.o_cvv + up128((size_t)kTsContactCap * 24);
+  P.stage_bytes = P.o_crp + up128((size_t)(P.cap_rows + 1) * 4);
   // + the row terms (cs) and transposed terms (tp) of a tile, double-buffered across tiles
   P.o_scratch = 128 + (size_t)kTsStages * P.stage_bytes;
   P.smem = P.o_scratch + kTsScratchBufs * 24 * (size_t)(P.cap_cs + P.cap_tp + kTsContactCap);
@@ -272,7 +268,6 @@ struct TsArgs {
   TsPlan P;
   const double* val;
   Bsr C;
-  const int2* crange;  // [ntiles] contact block range of each tile's rows (k_ts_crange), with C
   const double* v;
   double* y;
   double* part;
@@ -371,11 +366,9 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
     const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
     constexpr int D = kTsStages - 1;  // gathers trail the bulk copies by D tiles
     int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
-    int2 cg = make_int2(0, 0);  // the tile's contact block range (this Newton iteration's pattern)
     if (lane == 0 && count > 0) {
       d0 = __ldg(a.P.desc + first);
       d1 = __ldg(a.P.desc + first + 1);
-      if (crp) cg = __ldg(a.crange + first);
     }
     // iteration j: gather for tile j - D (its bulk copies were issued D iterations ago), then bulk
     // copies for tile j once the consumers have released its stage
@@ -396,16 +389,6 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         if (crp) {
           int* cr = reinterpret_cast<int*>(S + a.P.o_crp);
           for (int q = lane; q <= R; q += 32) cp_async4(cr + q, crp + r0 + q);
-          // v at the staged contact blocks' columns (the columns arrived with the bulk copies)
-          const int2 ck = __ldg(a.crange + first + k * G);
-          const int ncs = min(ck.y - ck.x, kTsContactCap);
-          const int* ccol = reinterpret_cast<const int*>(S + a.P.o_ccol) +
-                            ((reinterpret_cast<uintptr_t>(a.C.col + ck.x) & 15) >> 2);
-          double* cvv = reinterpret_cast<double*>(S + a.P.o_cvv);
-          for (int e = lane; e < 3 * ncs; e += 32) {
-            const int q = e / 3, c = e - 3 * q;
-            cp_async8(cvv + e, a.v + 3 * (size_t)ccol[q] + c);
-          }
         }
         if (lane == 0) {
           uintptr_t xa0, xe1, xa, xe;
@@ -429,32 +412,14 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
           uintptr_t xa0, xe1, xa, xe;
           v_span(d0.z, d1.z, xa0, xe1, xa, xe);
           const unsigned bm = (unsigned)(m1 - m0), bv = (unsigned)(ve1 - va0), bx = (unsigned)(xe1 - xa0);
-          unsigned bcv = 0, bcc = 0;
-          uintptr_t cv0 = 0, cc0 = 0;
-          const int ce = min(cg.y, cg.x + kTsContactCap);
-          if (ce > cg.x) {
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.C.val + 9 * (size_t)cg.x);
-            const uintptr_t a1 = reinterpret_cast<uintptr_t>(a.C.val + 9 * (size_t)ce);
-            cv0 = a0 & ~(uintptr_t)15;
-            bcv = (unsigned)(((a1 + 15) & ~(uintptr_t)15) - cv0);
-            const uintptr_t c0 = reinterpret_cast<uintptr_t>(a.C.col + cg.x);
-            const uintptr_t c1 = reinterpret_cast<uintptr_t>(a.C.col + ce);
-            cc0 = c0 & ~(uintptr_t)15;
-            bcc = (unsigned)(((c1 + 15) & ~(uintptr_t)15) - cc0);
-          }
-          mbar_expect_tx(fb, bm + bv + bx + bcv + bcc);
+          mbar_expect_tx(fb, bm + bv + bx);
           bulk_g2s(S + a.P.o_meta, a.P.meta + m0, bm, fb, pf);
           bulk_g2s(S + a.P.o_val, reinterpret_cast<const void*>(va0), bv, fb, pf);
           if (bx) bulk_g2s(S + a.P.o_vt, reinterpret_cast<const void*>(xa0), bx, fb, pl);
-          if (bcv) {
-            bulk_g2s(S + a.P.o_ccv, reinterpret_cast<const void*>(cv0), bcv, fb, pf);
-            bulk_g2s(S + a.P.o_ccol, reinterpret_cast<const void*>(cc0), bcc, fb, pf);
-          }
           if (j + 1 < count) {  // next tile's descriptors, off the critical path
             const int t = first + (j + 1) * G;
             d0 = __ldg(a.P.desc + t);
             d1 = __ldg(a.P.desc + t + 1);
-            if (crp) cg = __ldg(a.crange + t);
           }
         }
         __syncwarp();
@@ -507,22 +472,21 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         }
       }
       TS_T(6)
-      // contact blocks of the tile's rows (one contiguous range of the row-sorted contact BSR, staged
-      // with the tile by the producer): one thread per block, C_s v_col -> cc[s] (the first
-      // kTsContactCap of the tile; the rest, rare, are taken by their row thread in phase 2)
+      // contact blocks of the tile's rows (one contiguous range of the row-sorted contact BSR): one
+      // thread per block, C_s v_col -> cc[s] (the first kTsContactCap of the tile; the rest, rare,
+      // are taken by their row thread in phase 2)
       const int* cr = reinterpret_cast<const int*>(S + a.P.o_crp);
       double* cc = tp + 3 * (size_t)a.P.cap_tp;
       const int c0r = crp ? cr[0] : 0;
       const int ncc = crp ? min(cr[R] - c0r, kTsContactCap) : 0;
-      const double* ccv = reinterpret_cast<const double*>(S + a.P.o_ccv) +
-                          ((reinterpret_cast<uintptr_t>(a.C.val + 9 * (size_t)c0r) & 15) >> 3);
-      const double* cvv = reinterpret_cast<const double*>(S + a.P.o_cvv);
       for (int e = ct; e < ncc; e += kTsConsumers) {
-        const double* A = ccv + 9 * e;
+        const size_t s2 = (size_t)(c0r + e);
+        const double* A = a.C.val + 9 * s2;
+        const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
         double m[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) m[k] = A[k];
-        const double c0 = cvv[3 * e], c1 = cvv[3 * e + 1], c2 = cvv[3 * e + 2];
+        for (int k = 0; k < 9; ++k) m[k] = __ldg(A + k);
+        const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);
         cc[3 * e] = fma(m[2], c2, fma(m[1], c1, m[0] * c0));
         cc[3 * e + 1] = fma(m[5], c2, fma(m[4], c1, m[3] * c0));
         cc[3 * e + 2] = fma(m[8], c2, fma(m[7], c1, m[6] * c0));
@@ -618,18 +582,6 @@ k_ts_combine(int n, const int* __restrict__ pin_ptr, const double* __restrict__ 
   }
 }
 
-__global__ void k_ts_crange(int ntiles, const int4* __restrict__ desc, const int* __restrict__ crp,
-                            int2* __restrict__ out) {
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x)
-    out[t] = make_int2(crp[desc[t].z], crp[desc[t + 1].z]);
-}
-
-void launch_ts_crange(cudaStream_t st, const TsPlan& P, const int* contact_row_ptr) {
-  if (P.ntiles <= 0 || !contact_row_ptr) return;
-  k_ts_crange<<<ceil_div(P.ntiles, 256), 256, 0, st>>>(P.ntiles, P.desc, contact_row_ptr, P.crange);
-  CK(cudaGetLastError());
-}
-
 namespace {
 template <bool DOT>
 int ts_grid(const TsPlan& P) {
@@ -658,7 +610,7 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
                     bool combine) {
   const int g = ts_grid<false>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  TsArgs a{*S.ts, S.val, C, S.ts->crange, v, y, part, nullptr, nullptr, nullptr, nullptr, nullptr};
+  TsArgs a{*S.ts, S.val, C, v, y, part, nullptr, nullptr, nullptr, nullptr, nullptr};
 #ifdef BAL_TS_TIMING
   unsigned long long z[16] = {0};
   CK(cudaMemcpyToSymbolAsync(g_ts_timing, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
@@ -684,7 +636,7 @@ void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const doubl
                         double* dpart, unsigned* counter, PcgScal* sc, const double* upart, double* hist) {
   const int g = ts_grid<true>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  TsArgs a{*S.ts, S.val, C, S.ts->crange, u, w, part, dpart, counter, sc, upart, hist};
+  TsArgs a{*S.ts, S.val, C, u, w, part, dpart, counter, sc, upart, hist};
   k_spmv_ts<true><<<g, kTsThreads, S.ts->smem, st>>>(a);
   CK(cudaGetLastError());
 }

@@ -37,7 +37,7 @@ constexpr int kTsStages = BAL_TS_STAGES;
 #endif
 constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;
 #ifndef BAL_TS_CONTACT_CAP
-#define BAL_TS_CONTACT_CAP 192
+#define BAL_TS_CONTACT_CAP 384
 #endif
 constexpr int kTsContactCap = BAL_TS_CONTACT_CAP;  // contact blocks per tile computed block-parallel  // 2: consecutive tiles' scratch double-buffered
 constexpr int kTsMaxRows = kTsConsumers;  // one consumer thread per owned row
@@ -98,8 +98,6 @@ struct TsPlan {
   double* part = nullptr;              // [3 nslots] work buffer of the partials (owned by the ctx)
   int cap_nb = 0, cap_rows = 0, cap_cs = 0, cap_tp = 0;
   size_t o_crp = 0;  // contact row pointers of the tile (cp.async with the out-of-tile v)
-  size_t o_ccv = 0, o_ccol = 0, o_cvv = 0;  // staged contact blocks, their columns, v there
-  int2* crange = nullptr;  // [ntiles] per Newton iteration: contact block range of each tile
   size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
   long long meta_bytes = 0, ncross_total = 0;
 };
@@ -109,14 +107,11 @@ struct TsHost {  // host build of a TsPlan (ts_build)
   std::vector<unsigned char> meta;
   int ntiles = 0, nslots = 0, cap_nb = 0, cap_rows = 0, cap_x = 0, cap_meta = 0, cap_cs = 0, cap_tp = 0;
   long long ncross_total = 0;
-  size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, o_crp = 0, o_ccv = 0, o_ccol = 0, o_cvv = 0, stage_bytes = 0,
-         o_scratch = 0, smem = 0;
+  size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, o_crp = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
 };
 // lower CSR (lrow[N+1], lcol: lower + diagonal blocks, ascending column) -> plan; false = unusable
 bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, TsHost& P);
 int ts_prepare(const TsPlan& P);  // grid (0 = does not fit); call outside stream capture
-// per Newton iteration, after the contact pattern is built: each tile's contact block range
-void launch_ts_crange(cudaStream_t st, const TsPlan& P, const int* contact_row_ptr);
 bool ts_usable(const Bsr& S);
 // y = A v: owned rows to y, cross-tile partials to part; combine = add the partials into y
 void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v, double* y, double* part,
@@ -151,9 +146,15 @@ struct PcgScal {
   double rz, pq, alpha, beta, rr, bnorm, tol, dec;
   int k, stop, done, max_iters, window, hcap;  // hist[0..hcap) = ||r_k||, hist[hcap..) = phi_0 - phi_k
   int lit;      // BAL_PCG_LITERAL_STALL: Q15 residual-minimum stagnation test instead of R-PCG1
+  double stall_rel;  // R-PCG1 threshold (kStallRel)
   double pmin;  // literal test: min ||r_j|| over j <= k - window (maintained incrementally)
 };
 constexpr double kStallRel = 1e-10;  // DESIGN.md R-PCG1
+// R-PCG1 threshold; BAL_STALL_REL overrides it (experiments)
+inline double stall_rel() {
+  static const double v = getenv("BAL_STALL_REL") ? atof(getenv("BAL_STALL_REL")) : kStallRel;
+  return v;
+}
 // warm-start per-group scalars
 struct GrpScal {
   double rz[kMaxGroups], pq[kMaxGroups], alpha[kMaxGroups], beta[kMaxGroups], rr[kMaxGroups],

@@ -242,6 +242,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.hcap = hcap;
   h.lit = (c->prm.flags & BAL_PCG_LITERAL_STALL) ? 1 : 0;
   h.pmin = INFINITY;
+  h.stall_rel = stall_rel();
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
   if (ts_usable(S)) {

@@ -560,6 +560,7 @@ int pcg_solve_dist(bal_ctx* c, const double* rhs, const double* x0, double* x_ou
   h.hcap = hcap;
   h.lit = (c->prm.flags & BAL_PCG_LITERAL_STALL) ? 1 : 0;
   h.pmin = INFINITY;
+  h.stall_rel = stall_rel();
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   tp_halo(c, c->px.ptr);
   launch_spmv(st, So, C, c->px.ptr, c->pq.ptr);

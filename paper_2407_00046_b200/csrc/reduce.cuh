@@ -71,7 +71,7 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
       stall = wmin >= sc->pmin;
     } else {  // R-PCG1
       const double* dh = hist + sc->hcap;
-      stall = dh[k] - dh[k - W] <= kStallRel * dh[k];
+      stall = dh[k] - dh[k - W] <= sc->stall_rel * dh[k];
     }
     if (stall) {
       sc->stop = 1;
