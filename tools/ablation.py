@@ -1,9 +1,10 @@
 """NEXT-1 ablations on the same kernels: warm start on/off (Fig. warm
-start), BAL vs plain inexact-Newton IPC (A' = empty, sigma = sigma^0).  Runs whole frames of
-a scene through bal_frame_* with each flag set and prints per-variant totals as JSON lines.
+start), BAL vs plain inexact-Newton IPC (A' = empty, sigma = sigma^0), the capped and the
+min readings of the sigma schedule (Alg. 1 line 16).  Runs whole frames of a scene through
+bal_frame_* with each flag set and prints per-variant totals as JSON lines.
 
-    python tools/ablation.py c1 [frames]            # C1 cubes, all frames
-    python tools/ablation.py c4 [newton_iters]      # C4: the first K Newton iterations of frame 0
+    python tools/ablation.py c1|c2|c3 [frames]      # whole frames
+    python tools/ablation.py c4 [newton_iters]      # C4 drop start: the first K Newton iterations of frame 0
 """
 import json
 import os
@@ -16,7 +17,8 @@ import paper_2407_00046_b200 as bal  # noqa: E402
 import scenes  # noqa: E402
 
 VARIANTS = {"bal+warmstart": 0, "bal, no warm start": bal.BAL_NO_WARMSTART,
-            "inexact Newton (no AL)": bal.BAL_NO_AUGLAG}
+            "inexact Newton (no AL)": bal.BAL_NO_AUGLAG, "sigma cap 1e8 sigma0": bal.BAL_SIGMA_CAP,
+            "sigma min(1.2 sigma, 100 sigma0)": bal.BAL_SIGMA_MIN}
 
 
 def run(sc, flags, frames=None, newton=None):
@@ -50,9 +52,13 @@ def run(sc, flags, frames=None, newton=None):
 def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "c1"
     k = int(sys.argv[2]) if len(sys.argv) > 2 else (10 if which == "c1" else 20)
-    sc = scenes.make_cubes(1) if which == "c1" else scenes.make_puffer_net(seed=4)
+    sc = {"c1": lambda: scenes.make_cubes(1), "c2": lambda: scenes.make_armadillo_like(2),
+          "c3": lambda: scenes.make_impact(3), "c4": lambda: scenes.make_puffer_net(seed=4)}[which]()
     for name, fl in VARIANTS.items():
-        r = run(sc, fl, frames=k) if which == "c1" else run(sc, fl, newton=k)
+        try:
+            r = run(sc, fl, newton=k) if which == "c4" else run(sc, fl, frames=k)
+        except bal.BalError as e:  # a variant that fails (e.g. NaN) is reported, not fatal
+            r = {"error": str(e)}
         print(json.dumps({"scene": which, "variant": name, **r}), flush=True)
 
 
