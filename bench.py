@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", default="c4", choices=["c4", "c4-drop", "c1", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--fp32-matrix", action="store_true",
+                    help="NEXT-3 variant: SpMV streams FP32-rounded static blocks (FP64 arithmetic)")
     return ap.parse_args()
 
 
@@ -302,13 +304,14 @@ def run_ours(args):
     # every SpMV + one all-reduce per PCG iteration; strong scaling of the one C4 problem).
     # BAL_BENCH_REPLICAS=1: N independent replicas instead (weak scaling, no data-path collective).
     replicas = world > 1 and os.environ.get("BAL_BENCH_REPLICAS") == "1"
+    flags = bal.BAL_FP32_MATRIX if args.fp32_matrix else 0
     shared = world > 1 and not replicas
     if shared:
         obj = [bal.bal_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        ctx = bal.bal_init(sc, device=local, rank=rank, world=world, nccl_id=obj[0])
+        ctx = bal.bal_init(sc, device=local, rank=rank, world=world, nccl_id=obj[0], flags=flags)
     else:
-        ctx = bal.bal_init(sc, device=local)
+        ctx = bal.bal_init(sc, device=local, flags=flags)
     stream = torch.cuda.current_stream(dev)
     bal.bal_set_stream(ctx, stream)
     x = torch.as_tensor(sc["x0"].ravel(), device=dev)
@@ -393,9 +396,9 @@ def run_ours(args):
         if shared:
             obj = [bal.bal_nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
-            ctx2 = bal.bal_init(sc, device=local, params=prm, rank=rank, world=world, nccl_id=obj[0])
+            ctx2 = bal.bal_init(sc, device=local, params=prm, rank=rank, world=world, nccl_id=obj[0], flags=flags)
         else:
-            ctx2 = bal.bal_init(sc, device=local, params=prm)
+            ctx2 = bal.bal_init(sc, device=local, params=prm, flags=flags)
         xh = run.x.detach().cpu().numpy().copy()
         vh = run.v.detach().cpu().numpy().copy()
         torch.cuda.synchronize()
@@ -444,7 +447,8 @@ def run_ours(args):
         "metric": METRIC, "value": pcg_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if shared else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64 (SpMV static blocks stored f32)" if args.fp32_matrix else "f64",
+        "data": "synthetic",
         "config": {"workload": wl, "tets": int(len(sc["tets"])), "nodes": int(len(sc["rest_x"])),
                    "step": "one inexact-Newton iteration of Alg. 1 (constraint sets, stencils, assembly, warm "
                            "start, PCG, CCD line search, AL updates); frames continue across steps",

@@ -77,6 +77,10 @@ typedef struct { double E, nu, rho; } bal_material;
                                     * best ||r|| of the last window is no better than the best before it)
                                     * instead of DESIGN.md R-PCG1's CG-objective test (ablation) */
 
+#define BAL_FP32_MATRIX 256u /* NEXT-3 ("single-precision version"): the global PCG's SpMV streams the
+                              * stored static blocks rounded to FP32 (36 B instead of 72 B per block);
+                              * arithmetic, vectors, contact blocks, preconditioner and warm start stay FP64 */
+
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {
   double h;              /* time step (s) */

@@ -31,6 +31,7 @@ BAL_SIGMA_MIN = 16
 BAL_FRICTION_NO_FREEZE = 32
 BAL_CCD_LITERAL = 64
 BAL_PCG_LITERAL_STALL = 128
+BAL_FP32_MATRIX = 256
 
 
 class bal_mesh(C.Structure):

@@ -70,7 +70,7 @@ struct ContactWork {
 };
 
 void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage, const double* mass,
-                   double inv_h2, const uint8_t* fixed, double* val, double* lval);
+                   double inv_h2, const uint8_t* fixed, double* val, double* lval, float* lval32 = nullptr);
 int build_contact_pattern(cudaStream_t st, ContactWork& w, int ns, const int* nodes, const uint8_t* fixed, int n,
                           const double* stage);
 void node_finalize(cudaStream_t st, int n, const double* x, const double* y, const double* mass, double inv_h2,

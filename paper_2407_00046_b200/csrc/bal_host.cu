@@ -11,7 +11,7 @@
 
 using namespace bal;
 
-void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, cudaStream_t st) {
+void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int val_bytes, cudaStream_t st) {
   ready = false;
   if (getenv("BAL_SPMV_GENERIC") != nullptr || N <= 0) return;
   int dev = 0, smem_max = 0;
@@ -26,7 +26,7 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
   const size_t per_cta = std::min<size_t>((size_t)smem_max, (size_t)smem_sm / kTsMinBlocks) - 1024;
   for (int budget : {env > 0 ? env : 768, 704, 640, 576, 512, 448, 384, 320, 288, 256, 224, 192, 160, 128, 96, 64}) {
-    if (!ts_build(N, lrow, lcol, budget, H)) return;
+    if (!ts_build(N, lrow, lcol, budget, val_bytes, H)) return;
     if (H.smem <= per_cta) {
       ok = true;
       break;
@@ -59,6 +59,7 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   plan.stage_bytes = H.stage_bytes;
   plan.o_scratch = H.o_scratch;
   plan.cap_nb = H.cap_nb;
+  plan.val_bytes = H.val_bytes;
   plan.cap_cs = H.cap_cs;
   plan.cap_tp = H.cap_tp;
   plan.smem = H.smem;
@@ -83,6 +84,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.row_ptr = lb_lrow.ptr;
     b.col = lb_lcol.ptr;
     b.val = lb_lval.ptr;
+    b.val32 = lb_lval32.ptr;
     b.m_row_ptr = lb_urow.ptr;
     b.m_pos = lb_upos.ptr;
     b.m_col = lb_ucol.ptr;
@@ -93,6 +95,7 @@ bal::Bsr bal_ctx::static_bsr() const {
     b.row_ptr = sp.l_row_ptr;
     b.col = sp.l_col;
     b.val = lval.ptr;
+    b.val32 = lval32.ptr;
     b.m_row_ptr = sp.u_row_ptr;
     b.m_pos = sp.u_pos;
     b.m_col = sp.u_col;
@@ -428,7 +431,8 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     c->sp_sym = spmv_symmetric_enabled();
     if (c->sp_sym) {
       c->lval.reserve(9 * (size_t)std::max(c->sp.nl, 1) + 2);  // + 16 B slack for the bulk copies
-      c->sp_ts.build(N, lrow, lcol, st);
+      if (c->prm.flags & BAL_FP32_MATRIX) c->lval32.reserve(9 * (size_t)std::max(c->sp.nl, 1) + 4);
+      c->sp_ts.build(N, lrow, lcol, (c->prm.flags & BAL_FP32_MATRIX) ? 36 : 72, st);
     }
     for (int r0 = 0; r0 < N; r0 += kSpmvTileRows)
       c->sp.tile_cap_full = std::max(c->sp.tile_cap_full,
@@ -491,7 +495,7 @@ void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
   }
   const double inv_h2 = 1.0 / (c->prm.h * c->prm.h);
   gather_static(st, c->sp, c->stage_e.ptr, c->mass.ptr, inv_h2, c->fixed.ptr, c->sval.ptr,
-                c->sp_sym ? c->lval.ptr : nullptr);
+                c->sp_sym ? c->lval.ptr : nullptr, c->sp_sym ? c->lval32.ptr : nullptr);
   build_contact_pattern(st, c->cw, ns, c->nodes_c.ptr, c->fixed.ptr, N, c->stage_c.ptr);
   if (ns == 0) c->cw.nslots = 0;
   node_finalize(st, N, x, y, c->mass.ptr, inv_h2, c->fixed.ptr, c->sp, c->grad_e.ptr, c->lbar_e.ptr, c->sval.ptr,
@@ -711,7 +715,12 @@ bal_status bal_load_bsr(bal_ctx* c, const bal_bsr_host* b) {
       c->lb_upos.upload(upos.data(), std::max<size_t>(upos.size(), 1), st);
       c->lb_ucol.upload(ucol.data(), std::max<size_t>(ucol.size(), 1), st);
       lcol.resize(lcol.size() - 8);
-      c->lb_ts.build(N, lrow, lcol, st);
+      if (c->prm.flags & BAL_FP32_MATRIX) {  // FP32 copy of the loaded blocks (rounded once)
+        std::vector<float> lv32(lv.begin(), lv.end());
+        lv32.resize(lv32.size() + 4, 0.f);
+        c->lb_lval32.upload(lv32.data(), lv32.size(), st);
+      }
+      c->lb_ts.build(N, lrow, lcol, (c->prm.flags & BAL_FP32_MATRIX) ? 36 : 72, st);
     }
 
     // diagonal inverse from the loaded blocks (host: test path only)

@@ -18,7 +18,7 @@ struct TsDev {
   bal::TsPlan plan;
   bool ready = false;
   // lower CSR (lrow[N+1], lcol) -> plan on the device; ready = false when the kernel cannot be used
-  void build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, cudaStream_t st);
+  void build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int val_bytes, cudaStream_t st);
   void wire(bal::Bsr& b) const {
     if (ready) b.ts = &plan;
   }
@@ -70,6 +70,7 @@ struct bal_ctx {
   bal::DevBuf<double> sval;
   bal::DevBuf<int> sp_lpos, sp_lrow, sp_lcol, sp_urow, sp_upos, sp_ucol;  // symmetric SpMV copy
   bal::DevBuf<double> lval;
+  bal::DevBuf<float> lval32;  // BAL_FP32_MATRIX: FP32 copy of the stored blocks for k_spmv_ts
   bool sp_sym = false;
   TsDev sp_ts;
   // ---- elastic stencils
@@ -93,6 +94,7 @@ struct bal_ctx {
   // symmetric copy of the loaded system (lower + diagonal blocks, mirror index, SpMV plan)
   bal::DevBuf<int> lb_lrow, lb_lcol, lb_urow, lb_upos, lb_ucol;
   bal::DevBuf<double> lb_lval;
+  bal::DevBuf<float> lb_lval32;
   int lb_nl = 0, lb_nu = 0;
   TsDev lb_ts;
   // ---- PCG
@@ -118,7 +120,10 @@ struct bal_ctx {
     const double n = N;
     const double E = loaded_bsr ? 0.5 * (lb_nnzb - N) : 0.5 * (sp.nnzb - N);
     const double Cb = loaded_bsr ? 0.0 : 0.5 * (cw.nslots - cw.nrows);
-    return 72.0 * n + 76.0 * E + 4.0 * (n + 1) + 80.0 * Cb + 48.0 * n;
+    // values at the stored precision (BAL_FP32_MATRIX: 36 B per static block; contacts FP64)
+    const TsDev& ts = loaded_bsr ? lb_ts : sp_ts;
+    const double vb = ts.ready ? ts.plan.val_bytes : 72.0;
+    return vb * n + (vb + 4.0) * E + 4.0 * (n + 1) + 80.0 * Cb + 48.0 * n;
   }
   // bytes the SpMV kernel as configured must move at minimum: the tile-symmetric kernel streams
   // lower + diagonal values (72 B), the tile metadata, v rows, out-of-tile v, y rows and partials;
@@ -130,7 +135,7 @@ struct bal_ctx {
     const double contact = cc > 0 ? 76.0 * cc + 4.0 * (n + 1) : 0.0;
     const TsDev& ts = loaded_bsr ? lb_ts : sp_ts;
     if (ts.ready)
-      return 72.0 * (loaded_bsr ? lb_nl : sp.nl) + (double)ts.plan.meta_bytes + 48.0 * n +
+      return (double)ts.plan.val_bytes * (loaded_bsr ? lb_nl : sp.nl) + (double)ts.plan.meta_bytes + 48.0 * n +
              24.0 * (double)ts.plan.ncross_total + 24.0 * ts.plan.nslots + contact;
     if (loaded_bsr) return 76.0 * lb_nnzb + 4.0 * (n + 1) + 48.0 * n;
     const double stat = sp_sym ? 76.0 * sp.nl + 8.0 * sp.nu + 8.0 * (n + 1) : 76.0 * sp.nnzb + 4.0 * (n + 1);

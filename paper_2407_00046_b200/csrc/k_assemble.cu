@@ -62,7 +62,7 @@ __global__ void k_gather_static(int nnzb, const int* __restrict__ slot_row, cons
                                 const int* __restrict__ slot_ptr, const int* __restrict__ slot_code,
                                 const double* __restrict__ stage, const double* __restrict__ mass, double inv_h2,
                                 const uint8_t* __restrict__ fixed, double* __restrict__ val,
-                                const int* __restrict__ lpos, double* __restrict__ lval) {
+                                const int* __restrict__ lpos, double* __restrict__ lval, float* __restrict__ lval32) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nnzb) return;
   const int i = slot_row[s], j = col[s];
@@ -86,6 +86,11 @@ __global__ void k_gather_static(int nnzb, const int* __restrict__ slot_row, cons
       double* ol = lval + 9 * (size_t)lp;
 #pragma unroll
       for (int t = 0; t < 9; ++t) ol[t] = acc[t];
+      if (lval32) {  // BAL_FP32_MATRIX: the SpMV's stored blocks rounded to FP32
+        float* o32 = lval32 + 9 * (size_t)lp;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) o32[t] = (float)acc[t];
+      }
     }
   }
 }
@@ -241,9 +246,9 @@ __global__ void k_node_finalize(int n, const double* __restrict__ x, const doubl
 
 // ---------------------------------------------------------------------------- host side
 void gather_static(cudaStream_t st, const StaticPattern& sp, const double* stage, const double* mass,
-                   double inv_h2, const uint8_t* fixed, double* val, double* lval) {
+                   double inv_h2, const uint8_t* fixed, double* val, double* lval, float* lval32) {
   k_gather_static<<<ceil_div(sp.nnzb, 256), 256, 0, st>>>(sp.nnzb, sp.slot_row, sp.col, sp.slot_ptr, sp.slot_code,
-                                                           stage, mass, inv_h2, fixed, val, sp.lpos, lval);
+                                                           stage, mass, inv_h2, fixed, val, sp.lpos, lval, lval32);
   CK(cudaGetLastError());
 }
 

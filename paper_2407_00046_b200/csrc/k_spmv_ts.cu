@@ -1,7 +1,8 @@
 // k_spmv_ts.cu -- tile-symmetric BSR3 SpMV with cross-tile partials (§5.1).
 //
 // y = (D + L + L^T + sum C_i + C_i^T) v with the static part stored symmetrically (the paper's D + L:
-// lower + diagonal blocks of every row, row order, 72 B values + 4 B per block) and the
+// lower + diagonal blocks of every row, row order, 72 B values (36 B with BAL_FP32_MATRIX) + 4 B
+// per block) and the
 // per-iteration contact part stored as full rows.
 //
 // The rows are cut into tiles of consecutive rows holding at most `budget` stored blocks (<= 256
@@ -129,8 +130,10 @@ BAL_HD size_t up128(size_t x) { return (x + 127) & ~(size_t)127; }
 }  // namespace
 
 // ------------------------------------------------------------------------------------------ plan
-bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, TsHost& P) {
+bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, int val_bytes,
+              TsHost& P) {
   P = TsHost();
+  P.val_bytes = val_bytes;
   if (N <= 0) return false;
   // tiles: maximal runs of consecutive rows with <= budget stored blocks and <= kTsMaxRows rows
   // (one phase-1 thread per row)
@@ -253,7 +256,7 @@ bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol,
   // shared-memory layout of one stage: metadata | values | v rows | out-of-tile v
   P.o_meta = 0;
   P.o_val = up128((size_t)P.cap_meta);
-  P.o_vt = P.o_val + up128((size_t)P.cap_nb * 72 + 32);
+  P.o_vt = P.o_val + up128((size_t)P.cap_nb * val_bytes + 32);
   P.o_xv = P.o_vt + up128((size_t)P.cap_rows * 24 + 32);
   P.o_crp = P.o_xv + up128((size_t)std::max(P.cap_x, 1) * 24);
   P.stage_bytes = P.o_crp + up128((size_t)(P.cap_rows + 1) * 4);
@@ -266,7 +269,7 @@ bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol,
 // ------------------------------------------------------------------------------------------ kernel
 struct TsArgs {
   TsPlan P;
-  const double* val;
+  const void* val;  // lower + diagonal blocks: double[9] (FP64) or float[9] (BAL_FP32_MATRIX)
   Bsr C;
   const double* v;
   double* y;
@@ -327,8 +330,9 @@ __device__ unsigned long long g_ts_timing[16];
 #define TS_T(k)
 #endif
 
-template <bool DOT>
+template <bool DOT, typename VT>
 __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsArgs a) {
+  const VT* aval = static_cast<const VT*>(a.val);
   if (DOT && a.sc->done) return;
 #ifdef BAL_TS_TIMING
   long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -406,8 +410,8 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
           unsigned char* S = stage(j);
           uint64_t* fb = full + j % kTsStages;
           const long long m0 = 16ll * d0.x, m1 = 16ll * d1.x;
-          const uintptr_t va = reinterpret_cast<uintptr_t>(a.val + 9 * (size_t)d0.y);
-          const uintptr_t ve = reinterpret_cast<uintptr_t>(a.val + 9 * (size_t)d1.y);
+          const uintptr_t va = reinterpret_cast<uintptr_t>(aval + 9 * (size_t)d0.y);
+          const uintptr_t ve = reinterpret_cast<uintptr_t>(aval + 9 * (size_t)d1.y);
           const uintptr_t va0 = va & ~(uintptr_t)15, ve1 = (ve + 15) & ~(uintptr_t)15;
           uintptr_t xa0, xe1, xa, xe;
           v_span(d0.z, d1.z, xa0, xe1, xa, xe);
@@ -437,8 +441,8 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       const unsigned char* S = stage(it);
       const TsMeta M(S + a.P.o_meta);
       const int R = M.h->R, nc = M.h->ncross, r0 = M.h->r0, s0 = M.h->s0, nb = M.h->nb;
-      const uintptr_t va = reinterpret_cast<uintptr_t>(a.val + 9 * (size_t)s0);
-      const double* vals = reinterpret_cast<const double*>(S + a.P.o_val + (va & 15));
+      const uintptr_t va = reinterpret_cast<uintptr_t>(aval + 9 * (size_t)s0);
+      const VT* vals = reinterpret_cast<const VT*>(S + a.P.o_val + (va & 15));
       uintptr_t xa0, xe1, xa, xe;
       v_span(r0, r0 + R, xa0, xe1, xa, xe);
       const double* vt = reinterpret_cast<const double*>(S + a.P.o_vt + (xa - xa0));
@@ -454,10 +458,10 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         const int bl = (int)(cd & 0xffu), jr = (int)((cd >> 8) & 0xffffu);
         const unsigned kind = cd >> 24;
         const double* vj = kind == 2u ? xv + 3 * jr : vt + 3 * jr;
-        const double* A = vals + 9 * q;
+        const VT* A = vals + 9 * q;
         double m[9];
 #pragma unroll
-        for (int k = 0; k < 9; ++k) m[k] = A[k];
+        for (int k = 0; k < 9; ++k) m[k] = (double)A[k];  // FP64 arithmetic either way
         const double j0 = vj[0], j1 = vj[1], j2 = vj[2];
         double* c3 = cs + 3 * (int)M.cpos[q];
         c3[0] = fma(m[2], j2, fma(m[1], j1, m[0] * j0));
@@ -583,18 +587,26 @@ k_ts_combine(int n, const int* __restrict__ pin_ptr, const double* __restrict__ 
 }
 
 namespace {
+template <bool DOT, typename VT>
+int ts_grid_t(const TsPlan& P) {
+  static int per_sm = -1;
+  static size_t smem = 0;
+  if (per_sm < 0 || smem != P.smem) {
+    CK(cudaFuncSetAttribute(k_spmv_ts<DOT, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_ts<DOT, VT>, kTsThreads, P.smem));
+    smem = P.smem;
+  }
+  if (per_sm <= 0) return 0;
+  return std::max(1, std::min(per_sm * num_sms(), P.ntiles));
+}
 template <bool DOT>
 int ts_grid(const TsPlan& P) {
-  static int per_sm[2] = {-1, -1};
-  static size_t smem[2] = {0, 0};
-  int& ps = per_sm[DOT ? 1 : 0];
-  if (ps < 0 || smem[DOT ? 1 : 0] != P.smem) {
-    CK(cudaFuncSetAttribute(k_spmv_ts<DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_spmv_ts<DOT>, kTsThreads, P.smem));
-    smem[DOT ? 1 : 0] = P.smem;
-  }
-  if (ps <= 0) return 0;
-  return std::max(1, std::min(ps * num_sms(), P.ntiles));
+  return P.val_bytes == 36 ? ts_grid_t<DOT, float>(P) : ts_grid_t<DOT, double>(P);
+}
+template <bool DOT>
+void ts_launch(int g, cudaStream_t st, const TsArgs& a) {
+  if (a.P.val_bytes == 36) k_spmv_ts<DOT, float><<<g, kTsThreads, a.P.smem, st>>>(a);
+  else k_spmv_ts<DOT, double><<<g, kTsThreads, a.P.smem, st>>>(a);
 }
 }  // namespace
 
@@ -610,12 +622,13 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
                     bool combine) {
   const int g = ts_grid<false>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  TsArgs a{*S.ts, S.val, C, v, y, part, nullptr, nullptr, nullptr, nullptr, nullptr};
+  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, v, y, part,
+           nullptr, nullptr, nullptr, nullptr, nullptr};
 #ifdef BAL_TS_TIMING
   unsigned long long z[16] = {0};
   CK(cudaMemcpyToSymbolAsync(g_ts_timing, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
 #endif
-  k_spmv_ts<false><<<g, kTsThreads, S.ts->smem, st>>>(a);
+  ts_launch<false>(g, st, a);
   CK(cudaGetLastError());
 #ifdef BAL_TS_TIMING
   CK(cudaMemcpyFromSymbolAsync(z, g_ts_timing, sizeof(z), 0, cudaMemcpyDeviceToHost, st));
@@ -636,8 +649,9 @@ void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const doubl
                         double* dpart, unsigned* counter, PcgScal* sc, const double* upart, double* hist) {
   const int g = ts_grid<true>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  TsArgs a{*S.ts, S.val, C, u, w, part, dpart, counter, sc, upart, hist};
-  k_spmv_ts<true><<<g, kTsThreads, S.ts->smem, st>>>(a);
+  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, u, w, part, dpart,
+           counter, sc, upart, hist};
+  ts_launch<true>(g, st, a);
   CK(cudaGetLastError());
 }
 

@@ -70,6 +70,7 @@ struct Bsr {
   const int* row_ptr = nullptr;
   const int* col = nullptr;
   const double* val = nullptr;
+  const float* val32 = nullptr;  // FP32 copy of the stored blocks (BAL_FP32_MATRIX; k_spmv_ts only)
   // Symmetric storage (the paper's D + L + L^T): when m_row_ptr is set, the stored part
   // holds only the lower blocks and the diagonal (col <= row), and row i additionally applies, for
   // every j > i in m_col[m_row_ptr[i] .. m_row_ptr[i+1]), the transpose of the stored block
@@ -97,6 +98,7 @@ struct TsPlan {
   const int* pin_ptr = nullptr;        // [n+1] partial slots targeting row j: [pin_ptr[j], pin_ptr[j+1])
   double* part = nullptr;              // [3 nslots] work buffer of the partials (owned by the ctx)
   int cap_nb = 0, cap_rows = 0, cap_cs = 0, cap_tp = 0;
+  int val_bytes = 72;  // 72: FP64 stored blocks; 36: FP32 (BAL_FP32_MATRIX, FP64 arithmetic)
   size_t o_crp = 0;  // contact row pointers of the tile (cp.async with the out-of-tile v)
   size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
   long long meta_bytes = 0, ncross_total = 0;
@@ -106,11 +108,13 @@ struct TsHost {  // host build of a TsPlan (ts_build)
   std::vector<long long> meta_off;
   std::vector<unsigned char> meta;
   int ntiles = 0, nslots = 0, cap_nb = 0, cap_rows = 0, cap_x = 0, cap_meta = 0, cap_cs = 0, cap_tp = 0;
+  int val_bytes = 72;
   long long ncross_total = 0;
   size_t o_meta = 0, o_val = 0, o_vt = 0, o_xv = 0, o_crp = 0, stage_bytes = 0, o_scratch = 0, smem = 0;
 };
 // lower CSR (lrow[N+1], lcol: lower + diagonal blocks, ascending column) -> plan; false = unusable
-bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, TsHost& P);
+bool ts_build(int N, const std::vector<int>& lrow, const std::vector<int>& lcol, int budget, int val_bytes,
+              TsHost& P);
 int ts_prepare(const TsPlan& P);  // grid (0 = does not fit); call outside stream capture
 bool ts_usable(const Bsr& S);
 // y = A v: owned rows to y, cross-tile partials to part; combine = add the partials into y

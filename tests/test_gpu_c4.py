@@ -266,3 +266,23 @@ def test_c4_settled_pcg_iterates(c4_settled):
     st = la.pcg_cg(A, b, np.zeros_like(b), Dinv, tol=0.0, window=10 ** 9, max_iters=20)
     assert s["iters"] == 20 == st.k
     assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
+
+
+def test_c4_settled_fp32_matrix_spmv():
+    """BAL_FP32_MATRIX on the bench workload: static blocks streamed in FP32, contact blocks FP64: the
+    product over every row equals the CSR product of (FP32-rounded static + FP64 contact) blocks."""
+    sc = scenes.make_puffer_net(seed=4, settled=True)
+    ctx = bal.bal_init(sc, flags=bal.BAL_FP32_MATRIX)
+    x = torch.as_tensor(sc["x0"].ravel(), device=DEV)
+    v0 = torch.as_tensor(sc["v0"].ravel(), device=DEV)
+    bal.bal_frame_begin(ctx, x, v0)
+    bal.bal_frame_iterate(ctx, 1)
+    out = bal.bal_get_system(ctx)
+    N = len(sc["x0"])
+    As = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
+    As.data = As.data.astype(np.float32).astype(np.float64)
+    A = As + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
+    v = np.random.default_rng(7).normal(size=3 * N)
+    yg = torch.empty(3 * N, dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    assert np.all(np.abs(_np(yg) - A @ v) <= 1e-12 * (abs(A) @ np.abs(v)) + 1e-300)

@@ -285,3 +285,34 @@ def test_friction_stencils_and_assembly_parity(cubes_state):
     assert (np.asarray(abs(Ag - Ao).sum(axis=1)).ravel() / rowscale).max() <= 1e-9
     ge = _np(out["grad"])
     assert np.linalg.norm(ge - asm["grad"]) <= 1e-9 * np.linalg.norm(asm["grad"])
+
+
+# --------------------------------------------------------------------------- NEXT-3 FP32 storage
+def test_fp32_matrix_spmv_and_pcg_parity(cubes_state):
+    """BAL_FP32_MATRIX ("single-precision version"): the global PCG's SpMV streams the stored
+    blocks rounded to FP32, arithmetic stays FP64.  The product equals the oracle's product with the
+    entrywise FP32-rounded matrix (1e-12 of |A32||v|; bitwise repeatable) and 20 PCG iterates match
+    the oracle's pcg_cg on that matrix with the FP64 block-Jacobi preconditioner (1e-10)."""
+    sc, o, x1, _ = cubes_state
+    pt, ee = cm.candidates(o.mesh, x1, x1, o.dhat)
+    keys, d = cm.constraint_set(x1, pt, ee, o.dhat)
+    asm = o.assemble(x1, oracle_state(o, x1, sigma=4e5), keys)
+    A, Dinv = asm["A"], asm["Dinv"]
+    A32 = A.copy()
+    A32.data = A32.data.astype(np.float32).astype(np.float64)
+    assert np.abs(A32 - A).max() > 0  # the rounding is visible
+    ctx = bal.bal_init(sc, flags=bal.BAL_FP32_MATRIX)
+    bal.bal_load_bsr(ctx, *csr_to_bsr(A, o.N))
+    v = np.random.default_rng(11).normal(size=3 * o.N)
+    yg = torch.empty(3 * o.N, dtype=torch.float64, device=DEV)
+    bal.bal_spmv(ctx, _t(v), yg)
+    assert np.all(np.abs(_np(yg) - A32 @ v) <= 1e-12 * (abs(A32) @ np.abs(v)) + 1e-300)
+    y2 = torch.empty_like(yg)
+    bal.bal_spmv(ctx, _t(v), y2)
+    assert torch.equal(yg, y2)
+    b = -asm["grad"]
+    xg = torch.empty(3 * o.N, dtype=torch.float64, device=DEV)
+    s = bal.bal_pcg(ctx, _t(b), _t(np.zeros(3 * o.N)), xg, warm_start=0, rel_tol=0.0, stall_window=0, max_iters=20)
+    st = la.pcg_cg(A32, b, np.zeros(3 * o.N), Dinv, tol=0.0, window=10 ** 9, max_iters=20)
+    assert s["iters"] == 20 == st.k
+    assert np.linalg.norm(_np(xg) - st.x) <= 1e-10 * np.linalg.norm(st.x)
