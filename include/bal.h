@@ -235,6 +235,12 @@ typedef struct {
   const double* contact_blocks; /* [n][10][9] */
   const double* contact_lbar;   /* [n] */
   const int32_t* contact_stencil_nodes; /* [n][4], -1 padded */
+  /* appended in round 2 (per-stencil parity of K2 / K3): the last n_friction_stencils of the
+   * n_contact_stencils entries above are the friction stencils D_j, in the order of
+   * bal_contact_state.friction_keys; contact_grad holds every stencil's gradient over its
+   * nodes (contact: grad of phi_i(d_i); friction: grad D_j) */
+  int32_t n_friction_stencils;
+  const double* contact_grad;   /* [n][12] */
 } bal_system_view;
 
 /* Assemble the Newton system at x (device [3N]) for the given contact state: elastic (K1),
@@ -242,6 +248,14 @@ typedef struct {
  * gradient, Lambda / e_j / groups and the block-Jacobi inverse. */
 bal_status bal_assemble(bal_ctx* ctx, const double* x, const bal_contact_state* cs,
                         bal_system_view* out_view);
+
+/* The active set A = {d < dhat} at device positions x [3N] as the GPU path builds it (Alg. 1
+ * l.2; LBVH broad phase P:449-462, feature-pair distance with type resolution Q27 /
+ * R-EE1, R-DUP1): keys_out HOST [5*max_n] (type, canonical nodes, -1 padded; sorted), d_out HOST
+ * [max_n] the distance of each key.  *n_out = |A|.  Errors: BAL_E_INVALID_ARG (also when
+ * |A| > max_n; *n_out then holds |A|). */
+bal_status bal_detect(bal_ctx* ctx, const double* x, int32_t* keys_out, double* d_out, int32_t max_n,
+                      int32_t* n_out);
 
 /* Views of the system the last Newton iteration (bal_step / bal_frame_iterate) or bal_assemble
  * assembled (same fields and validity as bal_assemble's out_view).  Errors: BAL_E_INVALID_ARG. */

@@ -152,11 +152,12 @@ class Oracle:
             cols.append(np.tile(dof, (1, 12)).ravel())
             vals.append(P.reshape(-1))
             out["elastic_P"] = P
+            out["elastic_g"] = g
             out["elastic_lbar"] = lb
         # contact
         uk, inA, inAp, mu, s = self.contact_stencil_set(x, keys_A, st)
         cs = cm.contact_stencils(x, uk, inA, inAp, mu, s, st["sigma"], self.dhat) if len(uk) else []
-        c_P, c_lb, c_ids = [], [], []
+        c_P, c_lb, c_ids, c_g = [], [], [], []
         for (ids, g, H, _d, _dp) in cs:
             P, wc = project_eigh(H[None])
             lb = wc.sum() / (3 * len(ids))  # Q18 over the stencil's support nodes (R-DUP1)
@@ -166,7 +167,9 @@ class Oracle:
             c_P.append(P[0])
             c_lb.append(lb)
             c_ids.append(ids)
+            c_g.append(g)
         out["contact_keys"], out["contact_P"], out["contact_lbar"] = uk, c_P, c_lb
+        out["contact_g"] = c_g
         out["contact_ids"] = c_ids
         out["contact_inA"], out["contact_inAp"] = inA, inAp
         # friction (PSD analytically; not projected, not in Lambda: Q17)
@@ -326,6 +329,15 @@ class Oracle:
                 a_ccd = ccdm.step_toi(x, P, cpt, cee, dhat,
                                       np.inf if self.flags & FLAG_CCD_LITERAL else 1e-2)
                 alpha = min(1.0, a_ccd)
+                ccd_sens = 0.0
+                if trace is not None and a_ccd < 1.0:
+                    # conditioning of alpha_CCD (trace only, DESIGN.md R-TRACE): relative change of
+                    # the TOI under a 1e-6 relative perturbation of the direction, the size by which
+                    # two PCG implementations' directions differ; a near-double cubic root amplifies it
+                    xi = np.random.default_rng(l).standard_normal(P.shape)
+                    a_pert = ccdm.step_toi(x, P * (1.0 + 1e-6 * xi), cpt, cee, dhat,
+                                           np.inf if self.flags & FLAG_CCD_LITERAL else 1e-2)
+                    ccd_sens = abs(a_pert - a_ccd) / a_ccd
                 L0, _n0, S0 = self.energy(x, st, cpt, cee)
                 halvings = 0
                 ls_margin = np.inf  # closest accept/reject decision to its threshold, relative to S
@@ -359,7 +371,7 @@ class Oracle:
                                   ws_iters=ws_it, pcg_iters=pst.k, pcg_stop=pst.stop, alpha_ccd=a_ccd,
                                   alpha=alpha, halvings=halvings, resumes=resumes, safeguard=safeguard,
                                   rel_e=en / e0, nA_margin=cm.activation_margin(x, pt, ee, dhat),
-                                  ls_margin=ls_margin, pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
+                                  ls_margin=ls_margin, ccd_sens=ccd_sens, pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
             if en <= float(p["newton_rel_tol"]) * e0:
                 x = x_new
                 converged = True

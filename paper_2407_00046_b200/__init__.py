@@ -327,6 +327,16 @@ def bal_assemble(ctx, x, active_keys=(), aprime_keys=(), aprime_mu=(), aprime_s=
     return _views(v, x.device)
 
 
+def bal_detect(ctx, x, max_n=1 << 20):
+    """GPU active set at device positions x: (keys int32 [n][5], d float64 [n])."""
+    keys = np.zeros((max_n, 5), np.int32)
+    d = np.zeros(max_n, np.float64)
+    n = C.c_int32(0)
+    _check(ctx, _lib.lib.bal_detect(ctx.handle, *_vecs(ctx, x), _lib.ptr(keys, C.c_int32), _lib.ptr(d, C.c_double),
+                                    max_n, C.byref(n)))
+    return keys[:n.value].copy(), d[:n.value].copy()
+
+
 def bal_get_system(ctx, device=None):
     """Views of the system the last Newton iteration or bal_assemble assembled (copies, dict of
     torch tensors as bal_assemble returns)."""
@@ -362,6 +372,8 @@ def _views(v, device):
         contact_blocks=view(v.contact_blocks, 90 * v.n_contact_stencils, torch.float64),
         contact_lbar=view(v.contact_lbar, v.n_contact_stencils, torch.float64),
         contact_stencil_nodes=view(v.contact_stencil_nodes, 4 * v.n_contact_stencils, torch.int32),
+        n_friction_stencils=int(v.n_friction_stencils),
+        contact_grad=view(v.contact_grad, 12 * v.n_contact_stencils, torch.float64),
     )
 
 

@@ -75,7 +75,8 @@ class bal_system_view(C.Structure):
                 ("diag_inv", C.c_void_p), ("grad", C.c_void_p), ("e_node", C.c_void_p), ("group", C.c_void_p),
                 ("n_elastic", C.c_int32), ("elastic_blocks", C.c_void_p), ("elastic_lbar", C.c_void_p),
                 ("n_contact_stencils", C.c_int32), ("contact_blocks", C.c_void_p), ("contact_lbar", C.c_void_p),
-                ("contact_stencil_nodes", C.c_void_p)]
+                ("contact_stencil_nodes", C.c_void_p), ("n_friction_stencils", C.c_int32),
+                ("contact_grad", C.c_void_p)]
 
 
 class bal_pcg_opts(C.Structure):
@@ -122,6 +123,7 @@ _sig = {
     "bal_frame_peek": (C.c_int, [C.c_void_p, C.POINTER(bal_step_stats)]),
     "bal_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(bal_contact_state), C.POINTER(bal_system_view)]),
     "bal_get_system": (C.c_int, [C.c_void_p, C.POINTER(bal_system_view)]),
+    "bal_detect": (C.c_int, [C.c_void_p, C.c_void_p, c_int_p, c_double_p, C.c_int32, C.POINTER(C.c_int32)]),
     "bal_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "bal_pcg": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(bal_pcg_opts),
                           C.POINTER(bal_pcg_stats)]),

@@ -531,6 +531,8 @@ static void fill_view(const bal_ctx* c, bal_system_view* v) {
   v->contact_blocks = c->stage_c.ptr;
   v->contact_lbar = c->lbar_c.ptr;
   v->contact_stencil_nodes = c->nodes_c.ptr;
+  v->n_friction_stencils = c->n_fric;
+  v->contact_grad = c->grad_c.ptr;
 }
 
 extern "C" {

@@ -777,6 +777,25 @@ bal_status bal_frame_peek(const bal_ctx* c, bal_step_stats* stats) {
   return BAL_OK;
 }
 
+bal_status bal_detect(bal_ctx* c, const double* x, int32_t* keys_out, double* d_out, int32_t max_n,
+                      int32_t* n_out) {
+  if (!c || !x || !n_out || max_n < 0 || (max_n > 0 && (!keys_out || !d_out))) return BAL_E_INVALID_ARG;
+  return guard_step(c, [&]() {
+    if (!c->sw) c->sw = new StepWork();
+    StepWork& w = *c->sw;
+    proximity(c, w, x);
+    const int n = w.cs_A.n;
+    *n_out = n;
+    if (n > max_n) throw StepFail(BAL_E_INVALID_ARG, "bal_detect: more constraints than max_n");
+    if (n) {
+      CK(cudaMemcpyAsync(keys_out, w.cs_A.keys.ptr, 5 * (size_t)n * sizeof(int), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaMemcpyAsync(d_out, w.cs_A.d.ptr, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return BAL_OK;
+  });
+}
+
 int32_t bal_get_trace(const bal_ctx* c, double* out, int32_t max_records) {
   if (!c || !out || max_records < 0) return BAL_E_INVALID_ARG;
   const int n = (int)(c->trace.size() / BAL_TRACE_FIELDS);

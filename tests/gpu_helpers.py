@@ -48,3 +48,69 @@ def oracle_state(o, x, y=None, sigma=1.0, ap_keys=None, ap_mu=None, ap_s=None):
                 ap_keys=np.zeros((0, 5), np.int64) if ap_keys is None else ap_keys,
                 ap_mu=np.zeros(0) if ap_mu is None else ap_mu, ap_s=np.zeros(0) if ap_s is None else ap_s,
                 fr_keys=None)
+
+
+def _node_pairs(ids):
+    ids = np.asarray(ids, np.int64)
+    k = len(ids)
+    return np.repeat(ids, k), np.tile(ids, k)
+
+
+def assembly_bounds(o, x, y, asm, contact_tol=(), friction=None, friction_tol=(), elastic_tol=1e-12):
+    """Per-slot and per-node error bounds of an assembled system (SURVEY c.4 "per slot"):
+    slot (a, b) may differ by sum_i tol_i ||P_i||_F over the stencils i that write it (each stencil is
+    determined to tol_i relative: 1e-12 for tets, the distance-cancellation bound for contact and
+    friction), node j's gradient by sum_i tol_i ||g_i|| plus 1e-12 of its inertia term.  Returns
+    (slot bound as N x N CSR, node bound [N])."""
+    N = o.N
+    rows, cols, vals = [], [], []
+    gb = np.zeros(N)
+    tets = o.mesh.tets
+    if "elastic_P" in asm:
+        nP = np.linalg.norm(asm["elastic_P"].reshape(len(tets), -1), axis=1)
+        ng = np.linalg.norm(asm["elastic_g"].reshape(len(tets), -1), axis=1)
+        rows.append(np.repeat(tets, 4, axis=1).ravel())
+        cols.append(np.tile(tets, (1, 4)).ravel())
+        vals.append(np.repeat(elastic_tol * nP, 16))
+        for k in range(4):
+            np.add.at(gb, tets[:, k], elastic_tol * ng)
+    for P, g, ids, t in zip(asm.get("contact_P", []), asm.get("contact_g", []), asm.get("contact_ids", []),
+                            contact_tol):
+        r, c = _node_pairs(ids)
+        rows.append(r), cols.append(c), vals.append(np.full(len(r), t * np.linalg.norm(P)))
+        gb[np.asarray(ids)] += t * np.linalg.norm(g)
+    for (ids, g, H), t in zip(friction or [], friction_tol):
+        r, c = _node_pairs(ids)
+        rows.append(r), cols.append(c), vals.append(np.full(len(r), t * np.linalg.norm(H)))
+        gb[np.asarray(ids)] += t * np.linalg.norm(g)
+    mh = o.mesh.mass / o.h ** 2
+    # inertia M(x - y)/h^2: x - y carries ~u |x| absolute error per coordinate
+    gb += mh * (1e-12 * np.linalg.norm(x - y, axis=1) + 4e-16 * np.abs(x).max())
+    rows.append(np.arange(N)), cols.append(np.arange(N)), vals.append(1e-15 * mh)
+    B = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(N, N)).tocsr()
+    B.sum_duplicates()
+    return B, gb
+
+
+def slot_errors(Ag, Ao, N):
+    """Frobenius norm of each 3x3 block of Ag - Ao as an N x N CSR."""
+    D = (Ag - Ao).tocsr()
+    D2 = D.multiply(D).tocoo()
+    S = sp.coo_matrix((D2.data, (D2.row // 3, D2.col // 3)), shape=(N, N)).tocsr()
+    S.sum_duplicates()
+    S.data = np.sqrt(S.data)
+    return S
+
+
+def check_assembly_bounds(Ag, Ao, ge, go, B, gb, N, fixed):
+    """Every slot of Ag within its bound B (entries of B absent from the pattern: exact 0 allowed
+    only for the identity rows / columns of fixed nodes, App. C); every free node's gradient within gb.
+    Returns the worst ratios (slot, gradient)."""
+    S = slot_errors(Ag, Ao, N).tocoo()
+    free_pair = ~(fixed[S.row] | fixed[S.col])
+    err = S.data[free_pair]
+    bnd = np.asarray(B[S.row[free_pair], S.col[free_pair]]).ravel()
+    slot_ratio = float(np.max(err / np.maximum(bnd, 1e-300))) if len(err) else 0.0
+    dg = np.linalg.norm((np.asarray(ge) - np.asarray(go)).reshape(N, 3), axis=1)
+    g_ratio = float(np.max(dg[~fixed] / np.maximum(gb[~fixed], 1e-300))) if np.any(~fixed) else 0.0
+    return slot_ratio, g_ratio

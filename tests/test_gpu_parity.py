@@ -4,7 +4,8 @@ import numpy as np
 import pytest
 
 import scenes
-from tests.gpu_helpers import (bsr_to_csr, csr_to_bsr, dinv_full, lower_blocks_to_full, oracle_state)
+from tests.gpu_helpers import (assembly_bounds, bsr_to_csr, check_assembly_bounds, csr_to_bsr, dinv_full,
+                               lower_blocks_to_full, oracle_state)
 
 pytestmark = pytest.mark.gpu
 
@@ -99,10 +100,12 @@ def test_contact_stencils_and_full_assembly_parity(cubes_state):
     nodes = _np(out["contact_stencil_nodes"]).reshape(-1, 4)
     blocks = _np(out["contact_blocks"]).reshape(-1, 90)
     lbg = _np(out["contact_lbar"])
-    assert len(nodes) == len(asm["contact_keys"])
+    cg = _np(out["contact_grad"]).reshape(-1, 12)
+    assert len(nodes) == len(asm["contact_keys"]) and out["n_friction_stencils"] == 0
     worst = 0.0
-    for i, (k, ids, P, lb) in enumerate(zip(asm["contact_keys"], asm["contact_ids"], asm["contact_P"],
-                                            asm["contact_lbar"])):
+    tols = []
+    for i, (k, ids, P, g, lb) in enumerate(zip(asm["contact_keys"], asm["contact_ids"], asm["contact_P"],
+                                               asm["contact_g"], asm["contact_lbar"])):
         n = len(ids)
         assert list(nodes[i, :n]) == list(ids) and np.all(nodes[i, n:] == -1)
         Hg = lower_blocks_to_full(blocks[i], n)
@@ -110,20 +113,21 @@ def test_contact_stencils_and_full_assembly_parity(cubes_state):
         # only determined to ~C*u*|x|/d relative (C = 18)
         dd = cm.key_distance(x, k[None])[0]
         tol = 1e-12 + 4e-15 * np.abs(x).max() / dd
+        tols.append(tol)
         err = np.linalg.norm(Hg - P) / max(np.linalg.norm(P), 1e-300)
-        worst = max(worst, err / tol)
+        gerr = np.linalg.norm(cg[i, :3 * n] - g) / max(np.linalg.norm(g), 1e-300)
+        worst = max(worst, err / tol, gerr / tol)
         assert lbg[i] == pytest.approx(lb, rel=tol, abs=1e-300)
     assert worst <= 1.0, worst
     N = o.N
     Ag = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
     if out["contact_col"].numel():
         Ag = Ag + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
-    Ao = asm["A"]
-    rowscale = np.asarray(abs(Ao).sum(axis=1)).ravel() + 1e-300
-    dd = np.asarray(abs(Ag - Ao).sum(axis=1)).ravel() / rowscale
-    assert dd.max() <= 1e-9, dd.max()
-    ge = _np(out["grad"])
-    assert np.linalg.norm(ge - asm["grad"]) <= 1e-9 * np.linalg.norm(asm["grad"])
+    # per slot: |dA_ab| <= sum over the stencils writing (a, b) of tol_i ||P_i|| (c.4), and per node
+    # for the gradient -- in place of a row-relative 1e-9
+    B, gb = assembly_bounds(o, x, y, asm, contact_tol=tols)
+    rs, rg = check_assembly_bounds(Ag, asm["A"], _np(out["grad"]), asm["grad"], B, gb, N, o.mesh.fixed)
+    assert rs <= 1.0 and rg <= 1.0, (rs, rg)
     assert np.array_equal(_np(out["group"])[o.free], asm["groups"][o.free])
 
 
@@ -278,13 +282,35 @@ def test_friction_stencils_and_assembly_parity(cubes_state):
     out = bal.bal_assemble(ctx, _t(x), active_keys=keys, sigma=sigma, y=y, x_t=x_t,
                            friction=dict(keys=fk, gamma=G, n=n, lam=lam))
     N = o.N
+    # per-stencil friction (K3): D_j's gradient and (unprojected, PSD) Hessian over its nodes.  w =
+    # P_n Gamma (x - x_t) carries ~u|x| absolute error and H depends on w through f'(y)/y, f''(y) and
+    # w/|w| with y = |w| floored by the mollifier width eps (f is polynomial below eps, Q24), so a
+    # stencil is determined to ~u|x| / max(y, eps) relative
+    nf = out["n_friction_stencils"]
+    assert nf == len(fk) > 10
+    nc = len(asm["contact_keys"])
+    blocks = _np(out["contact_blocks"]).reshape(-1, 90)[nc:]
+    cg = _np(out["contact_grad"]).reshape(-1, 12)[nc:]
+    nodes = _np(out["contact_stencil_nodes"]).reshape(-1, 4)[nc:]
+    eps = float(o.p["eps_v"]) * o.h
+    ftol, worst = [], 0.0
+    for j, (ids, g, H) in enumerate(asm["friction"]):
+        kk = len(ids)
+        assert list(nodes[j, :kk]) == list(ids)
+        w = np.sum(G[j, :kk, None] * (x[ids] - x_t[ids]), axis=0)
+        w = w - np.dot(w, n[j]) * n[j]
+        tol = 1e-12 + 4e-15 * np.abs(x).max() / max(np.linalg.norm(w), eps)
+        ftol.append(tol)
+        e_h = np.linalg.norm(lower_blocks_to_full(blocks[j], kk) - H) / max(np.linalg.norm(H), 1e-300)
+        e_g = np.linalg.norm(cg[j, :3 * kk] - g) / max(np.linalg.norm(g), 1e-300)
+        worst = max(worst, e_h / tol, e_g / tol)
+    assert worst <= 1.0, worst
+    ctol = [1e-12 + 4e-15 * np.abs(x).max() / cm.key_distance(x, k[None])[0] for k in asm["contact_keys"]]
     Ag = bsr_to_csr(_np(out["static_row_ptr"]), _np(out["static_col"]), _np(out["static_val"]), N)
     Ag = Ag + bsr_to_csr(_np(out["contact_row_ptr"]), _np(out["contact_col"]), _np(out["contact_val"]), N)
-    Ao = asm["A"]
-    rowscale = np.asarray(abs(Ao).sum(axis=1)).ravel() + 1e-300
-    assert (np.asarray(abs(Ag - Ao).sum(axis=1)).ravel() / rowscale).max() <= 1e-9
-    ge = _np(out["grad"])
-    assert np.linalg.norm(ge - asm["grad"]) <= 1e-9 * np.linalg.norm(asm["grad"])
+    B, gb = assembly_bounds(o, x, y, asm, contact_tol=ctol, friction=asm["friction"], friction_tol=ftol)
+    rs, rg = check_assembly_bounds(Ag, asm["A"], _np(out["grad"]), asm["grad"], B, gb, N, o.mesh.fixed)
+    assert rs <= 1.0 and rg <= 1.0, (rs, rg)
 
 
 # --------------------------------------------------------------------------- NEXT-3 FP32 storage

@@ -144,7 +144,7 @@ def test_frame_slices_equal_bal_step():
 TRACE_INT = ("nA", "nAp", "rebuilt", "pcg_stop", "halvings", "resumes", "safeguard")
 
 
-NA_TIE, LS_TIE, PCG_TIE = 1e-9, 1e-12, 1e-4
+NA_TIE, LS_TIE, PCG_TIE, CCD_TIE = 1e-9, 1e-12, 1e-4, 1e-5
 
 
 def _trace_equal(tg, to, rel=1e-4):
@@ -154,7 +154,9 @@ def _trace_equal(tg, to, rel=1e-4):
     next iterate's ||e||, a small difference of large terms, to ~1e-5) -- up to the first Newton iteration whose decisions the oracle took within
     rounding of a threshold (a feature-pair distance within 1e-9 d_hat of d_hat, a line-search
     energy comparison within 1e-12 of its R-LS1 tolerance relative to the energy's magnitude sum,
-    or a PCG residual within 1e-4 of the App. B tolerance -- the GPU runs the Chronopoulos-Gear form
+    or a PCG residual within 1e-4 of the App. B tolerance, or an alpha_CCD that moves by more than
+    1e-5 relative when the direction is perturbed by 1e-6 relative, a near-double CCD cubic root
+    -- the GPU runs the Chronopoulos-Gear form
     of the oracle's textbook PCG, equal in exact arithmetic; their residual norms drift apart by
     rounding to ~1e-6 relative over tens of iterations):
     there either implementation may take either branch, and the later decisions of the step are
@@ -162,7 +164,8 @@ def _trace_equal(tg, to, rel=1e-4):
     iterations compared."""
     n = 0
     for g, o in zip(tg, to):
-        tie = o["nA_margin"] < NA_TIE or o["ls_margin"] < LS_TIE or o["pcg_margin"] < PCG_TIE
+        tie = (o["nA_margin"] < NA_TIE or o["ls_margin"] < LS_TIE or o["pcg_margin"] < PCG_TIE
+               or o["ccd_sens"] > CCD_TIE)
         if not tie or n == 0:
             for k in ("nA", "nAp", "rebuilt"):  # taken before any tie of this iteration can act
                 assert int(g[k]) == int(o[k]), (k, g, o)
