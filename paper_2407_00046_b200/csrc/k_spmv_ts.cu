@@ -77,6 +77,9 @@ BAL_D void cp_async8(void* dst, const void* src) {
 BAL_D void cp_async4(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+BAL_D void bulk_prefetch_l2(const void* src, unsigned bytes) {  // TMA prefetch into L2, no smem
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 BAL_D void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 BAL_D void cp_async_wait() {
@@ -279,6 +282,7 @@ struct TsArgs {
   PcgScal* sc;
   const double* upart;
   double* hist;
+  int cpref;  // producer prefetches each tile's contact range (values, columns) into L2
 };
 
 // sum of the 3-vectors p[3b .. 3e) into (s0, s1, s2), four independent partial sums (short
@@ -370,6 +374,7 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
     const unsigned long long pf = pol_evict_first(), pl = pol_evict_last();
     constexpr int D = kTsStages - 1;  // gathers trail the bulk copies by D tiles
     int4 d0 = make_int4(0, 0, 0, 0), d1 = d0;
+    int pc0 = 0, pc1 = 0;  // contact range of the tile whose bulk copies were issued last
     if (lane == 0 && count > 0) {
       d0 = __ldg(a.P.desc + first);
       d1 = __ldg(a.P.desc + first + 1);
@@ -379,6 +384,17 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
     for (int j = 0; j < count + D; ++j) {
       const int k = j - D;
       TS_T(1)
+      if (lane == 0 && pc1 > pc0) {
+        // the contact blocks of tile j - 1 (row-sorted contact BSR: one contiguous range) into L2, so
+        // the consumers' per-block loads of them one tile later hit L2 instead of HBM
+        const uintptr_t ca = reinterpret_cast<uintptr_t>(a.C.val + 9 * (size_t)pc0) & ~(uintptr_t)15;
+        const uintptr_t ce = (reinterpret_cast<uintptr_t>(a.C.val + 9 * (size_t)pc1) + 15) & ~(uintptr_t)15;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(ca), (unsigned)(ce - ca));
+        const uintptr_t ka = reinterpret_cast<uintptr_t>(a.C.col + pc0) & ~(uintptr_t)15;
+        const uintptr_t ke = (reinterpret_cast<uintptr_t>(a.C.col + pc1) + 15) & ~(uintptr_t)15;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(ka), (unsigned)(ke - ka));
+        pc0 = pc1 = 0;
+      }
       if (k >= 0) {
         mbar_wait(full + k % kTsStages, par(k));
         TS_T(2)
@@ -420,6 +436,10 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
           bulk_g2s(S + a.P.o_meta, a.P.meta + m0, bm, fb, pf);
           bulk_g2s(S + a.P.o_val, reinterpret_cast<const void*>(va0), bv, fb, pf);
           if (bx) bulk_g2s(S + a.P.o_vt, reinterpret_cast<const void*>(xa0), bx, fb, pl);
+          if (crp && a.cpref) {  // consumed at the next iteration (load latency off the critical path)
+            pc0 = __ldg(crp + d0.z);
+            pc1 = __ldg(crp + d1.z);
+          }
           if (j + 1 < count) {  // next tile's descriptors, off the critical path
             const int t = first + (j + 1) * G;
             d0 = __ldg(a.P.desc + t);
@@ -587,6 +607,10 @@ k_ts_combine(int n, const int* __restrict__ pin_ptr, const double* __restrict__ 
 }
 
 namespace {
+int ts_cpref() {  // BAL_TS_NO_CPREFETCH=1: no L2 prefetch of the contact ranges (ablation)
+  static const int on = getenv("BAL_TS_NO_CPREFETCH") ? 0 : 1;
+  return on;
+}
 template <bool DOT, typename VT>
 int ts_grid_t(const TsPlan& P) {
   static int per_sm = -1;
@@ -623,7 +647,7 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
   const int g = ts_grid<false>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
   TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, v, y, part,
-           nullptr, nullptr, nullptr, nullptr, nullptr};
+           nullptr, nullptr, nullptr, nullptr, nullptr, ts_cpref()};
 #ifdef BAL_TS_TIMING
   unsigned long long z[16] = {0};
   CK(cudaMemcpyToSymbolAsync(g_ts_timing, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
@@ -650,7 +674,7 @@ void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const doubl
   const int g = ts_grid<true>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
   TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, u, w, part, dpart,
-           counter, sc, upart, hist};
+           counter, sc, upart, hist, ts_cpref()};
   ts_launch<true>(g, st, a);
   CK(cudaGetLastError());
 }

@@ -1,11 +1,12 @@
 // pcg_dist.cu -- the partitioned multi-GPU solve: one process per GPU, contiguous
 // vertex (block-row) ranges aligned to the SpMV tile, replicated assembly, distributed warm start
 // (Q20) and global block-Jacobi PCG with the App. B policy (Q14-Q16).
-// Per PCG iteration: halo of p (boundary rows only, grouped ncclSend/ncclRecv with the ranks whose
-// rows the owned rows touch), SpMV of the owned rows with the fused p^T A p partial, ncclAllReduce of
-// p^T A p, the vector update of the owned rows with the r.z / r.r partials, ncclAllReduce of those,
-// the scalar step (beta, App. B stop test -- identical on every rank because the all-reduced sums
-// are), p = z + beta p.  The solution slices are all-gathered once per solve (zero-padded sum).
+// Global PCG in Chronopoulos-Gear form, per iteration: the vector update of the owned rows with the
+// (r,u), (r,r) partials, halo of u (boundary rows only, grouped ncclSend/ncclRecv with the ranks
+// whose rows the owned rows touch), SpMV of the owned rows with the fused (w,u) partial, ONE
+// ncclAllReduce of the three sums, the scalar step (App. B stop test, alpha, beta -- identical on
+// every rank because the all-reduced sums are).  The warm start keeps the textbook per-group
+// recurrences.  The solution slices are all-gathered once per solve (zero-padded sum).
 // A host transport (bal_dist.host_*) replaces NCCL for tests: same kernels, same data flow.
 #include <nccl.h>
 
@@ -50,96 +51,100 @@ __global__ void k_zero_outside(int n3, int a3, int b3, double* __restrict__ v) {
     if (j < a3 || j >= b3) v[j] = 0.0;
 }
 
-// global PCG init on the owned rows: r = b - A x0, z = M r, p = z; local (r.z, r.r, b.b)
+// Chronopoulos-Gear block-Jacobi PCG on the owned rows (the single-GPU recurrences of k_linalg.cu,
+// oracle.linalg.pcg_cg is the parity partner): ONE all-reduce per iteration, of (r,u), (r,r) (from
+// the update) and (w,u) (from the SpMV epilogue).
+// init: r = b - A x0, u = M^-1 r, p = s = 0; local (r,u), (r,r), (b,b) and x0.(b + r) (R-WS1 guard)
 __global__ void __launch_bounds__(kVecThreads)
-k_d_pcg_init(int r0, int r1, const double* __restrict__ b, const double* __restrict__ Ax0,
-             const double* __restrict__ dinv, double* __restrict__ r, double* __restrict__ z, double* __restrict__ p,
-             double* partials, unsigned* counter, double* red_loc) {
-  double loc[3] = {0.0, 0.0, 0.0};
+k_d_cg_init(int r0, int r1, const double* __restrict__ b, const double* __restrict__ Ax0,
+            const double* __restrict__ dinv, const double* __restrict__ x, double* __restrict__ r,
+            double* __restrict__ u, double* __restrict__ p, double* __restrict__ s, double* partials,
+            unsigned* counter, double* red_loc) {
+  double loc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
-    double rr[3], bb[3];
+    double rv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      bb[c] = b[3 * (size_t)i + c];
-      rr[c] = bb[c] - Ax0[3 * (size_t)i + c];
-      r[3 * (size_t)i + c] = rr[c];
+      const size_t j = 3 * (size_t)i + c;
+      const double bj = b[j];
+      rv[c] = bj - Ax0[j];
+      r[j] = rv[c];
+      p[j] = 0.0;
+      s[j] = 0.0;
+      loc[2] += bj * bj;
+      loc[3] += x[j] * (bj + rv[c]);
     }
-    double z0, z1, z2;
-    dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
-    z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
-    p[3 * (size_t)i] = z0; p[3 * (size_t)i + 1] = z1; p[3 * (size_t)i + 2] = z2;
-    loc[0] += rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
-    loc[1] += rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
-    loc[2] += bb[0] * bb[0] + bb[1] * bb[1] + bb[2] * bb[2];
+    double u0, u1, u2;
+    dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
+    u[3 * (size_t)i] = u0;
+    u[3 * (size_t)i + 1] = u1;
+    u[3 * (size_t)i + 2] = u2;
+    loc[0] += rv[0] * u0 + rv[1] * u1 + rv[2] * u2;
+    loc[1] += rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2];
   }
-  double tot[3];
-  if (last_block_reduce<3, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0)
-    for (int q = 0; q < 3; ++q) red_loc[q] = tot[q];
+  double tot[4];
+  if (last_block_reduce<4, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) red_loc[q] = tot[q];
 }
-__global__ void k_d_pcg_init_fin(const double* red_glob, PcgScal* sc, double* hist) {
-  sc->rz = red_glob[0];
-  sc->rr = red_glob[1];
-  sc->bnorm = sqrt(red_glob[2]);
+// [(r,u), (r,r)] of the last init / update, (w,u) of the SpMV epilogue and (b,b) -> the all-reduce buffer
+__global__ void k_d_cg_pack(const double* red_loc, const PcgScal* lsc, double* red_glob) {
+  red_glob[0] = red_loc[0];
+  red_glob[1] = red_loc[1];
+  red_glob[2] = lsc->pq;
+  red_glob[3] = red_loc[2];
+}
+// after the init's all-reduce: stop-test state, then the k = 0 scalars
+__global__ void k_d_cg_init_fin(PcgScal* sc, double* hist, const double* red_glob) {
+  sc->bnorm = sqrt(red_glob[3]);
   sc->k = 0;
   sc->stop = -1;
   sc->done = 0;
   sc->dec = 0.0;
-  hist[0] = sqrt(red_glob[1]);
-  hist[sc->hcap] = 0.0;
-  pcg_stop_check(sc, hist);
+  sc->rz = sc->alpha = sc->beta = 0.0;
+  cg_scalars(sc, hist, red_glob[0], red_glob[1], red_glob[2]);
 }
-
-// x += alpha p, r -= alpha q, z = M r on the owned rows; alpha = r.z / (all-reduced p^T A p)
-__global__ void __launch_bounds__(kVecThreads)
-k_d_pcg_update(int r0, int r1, const double* __restrict__ dinv, const double* __restrict__ p,
-               const double* __restrict__ q, double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
-               double* partials, unsigned* counter, const PcgScal* sc, const double* pq_glob, double* red_loc) {
+// after an iteration's all-reduce: App. B stop test on ||r_k||, beta_k, alpha_k (identical on every
+// rank: the all-reduced sums are)
+__global__ void k_d_cg_scal(PcgScal* sc, double* hist, const double* red_glob) {
   if (sc->done) return;
-  const double alpha = sc->rz / pq_glob[0];
+  cg_scalars(sc, hist, red_glob[0], red_glob[1], red_glob[2]);
+}
+// update k on the owned rows: p = u + beta p, s = w + beta s (= A p), x += alpha p, r -= alpha s,
+// u = M^-1 r; local (r,u), (r,r) for the next all-reduce
+__global__ void __launch_bounds__(kVecThreads)
+k_d_cg_update(int r0, int r1, const double* __restrict__ dinv, const double* __restrict__ w, double* __restrict__ u,
+              double* __restrict__ p, double* __restrict__ s, double* __restrict__ x, double* __restrict__ r,
+              double* partials, unsigned* counter, PcgScal* sc, double* red_loc) {
+  if (sc->done) return;
+  const double alpha = sc->alpha, beta = sc->beta;
   double loc[2] = {0.0, 0.0};
   for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
-    double rr[3];
+    double rv[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const size_t j = 3 * (size_t)i + c;
-      x[j] = x[j] + alpha * p[j];
-      rr[c] = r[j] - alpha * q[j];
-      r[j] = rr[c];
+      const double pj = u[j] + beta * p[j];
+      const double sj = w[j] + beta * s[j];
+      p[j] = pj;
+      s[j] = sj;
+      x[j] = x[j] + alpha * pj;
+      rv[c] = r[j] - alpha * sj;
+      r[j] = rv[c];
     }
-    double z0, z1, z2;
-    dinv_apply(dinv, i, rr[0], rr[1], rr[2], z0, z1, z2);
-    z[3 * (size_t)i] = z0; z[3 * (size_t)i + 1] = z1; z[3 * (size_t)i + 2] = z2;
-    loc[0] += rr[0] * z0 + rr[1] * z1 + rr[2] * z2;
-    loc[1] += rr[0] * rr[0] + rr[1] * rr[1] + rr[2] * rr[2];
+    double u0, u1, u2;
+    dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
+    u[3 * (size_t)i] = u0;
+    u[3 * (size_t)i + 1] = u1;
+    u[3 * (size_t)i + 2] = u2;
+    loc[0] += rv[0] * u0 + rv[1] * u1 + rv[2] * u2;
+    loc[1] += rv[0] * rv[0] + rv[1] * rv[1] + rv[2] * rv[2];
   }
   double tot[2];
   if (last_block_reduce<2, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
     red_loc[0] = tot[0];
     red_loc[1] = tot[1];
+    sc->k = sc->k + 1;  // read by the next k_d_cg_scal only
   }
-}
-// scalar step after the all-reduce: beta, the CG-objective decrease, history, App. B stop test
-__global__ void k_d_pcg_finish(PcgScal* sc, double* hist, const double* pq_glob, const double* rzrr_glob) {
-  if (sc->done) return;
-  const double alpha = sc->rz / pq_glob[0];
-  sc->pq = pq_glob[0];
-  sc->alpha = alpha;
-  sc->dec += 0.5 * alpha * sc->rz;
-  sc->beta = (sc->rz != 0.0) ? rzrr_glob[0] / sc->rz : 0.0;
-  sc->rz = rzrr_glob[0];
-  sc->rr = rzrr_glob[1];
-  const int k = sc->k + 1;
-  sc->k = k;
-  hist[k] = sqrt(rzrr_glob[1]);
-  hist[sc->hcap + k] = sc->dec;
-  pcg_stop_check(sc, hist);
-}
-__global__ void k_d_pcg_pupdate(int r0, int r1, const double* __restrict__ z, double* __restrict__ p,
-                                const PcgScal* sc) {
-  if (sc->done) return;
-  const double beta = sc->beta;
-  for (int j = 3 * r0 + blockIdx.x * blockDim.x + threadIdx.x; j < 3 * r1; j += gridDim.x * blockDim.x)
-    p[j] = z[j] + beta * p[j];
 }
 
 // ---- warm start (per-group PCG on A_GG, Q20) on the owned rows
@@ -447,6 +452,18 @@ void dist_destroy(bal_ctx* c) {
 // ------------------------------------------------------------------------------ solve
 namespace {
 
+// w = A u on the owned rows after the halo of u, its (w,u) partial, one all-reduce of the packed
+// scalars (4 with the init's (b,b))
+void cg_spmv_reduce(bal_ctx* c, const Bsr& So, const Bsr& C, int nred) {
+  DistState& d = c->dist;
+  cudaStream_t st = c->st;
+  tp_halo(c, c->pz.ptr);
+  launch_spmv_dot(st, So, C, c->pz.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, d.lscal.ptr);
+  k_d_cg_pack<<<1, 1, 0, st>>>(d.red.ptr, d.lscal.ptr, d.red.ptr + kRedHalf);
+  tp_allreduce(c, d.red.ptr + kRedHalf, nred);
+  c->launches += 2;
+}
+
 void run_global(bal_ctx* c, const Bsr& So, const Bsr& C, bal_pcg_stats* stats) {
   DistState& d = c->dist;
   cudaStream_t st = c->st;
@@ -455,19 +472,13 @@ void run_global(bal_ctx* c, const Bsr& So, const Bsr& C, bal_pcg_stats* stats) {
   constexpr int kB = 8;  // iterations enqueued between polls of the device stop flag
   while (true) {
     for (int it = 0; it < kB; ++it) {
-      tp_halo(c, c->pp.ptr);
-      launch_spmv_dot(st, So, C, c->pp.ptr, c->pq.ptr, c->partials.ptr, c->counter.ptr, d.lscal.ptr);
-      CK(cudaMemcpyAsync(red_glob, &d.lscal.ptr->pq, sizeof(double), cudaMemcpyDeviceToDevice, st));
-      tp_allreduce(c, red_glob, 1);
-      k_d_pcg_update<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, c->dinv.ptr, c->pp.ptr, c->pq.ptr, c->px.ptr,
-                                                         c->pr.ptr, c->pz.ptr, c->partials.ptr, c->counter.ptr,
-                                                         c->scal.ptr, red_glob, red_loc);
-      CK(cudaMemcpyAsync(red_glob + 1, red_loc, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      tp_allreduce(c, red_glob + 1, 2);
-      k_d_pcg_finish<<<1, 1, 0, st>>>(c->scal.ptr, c->hist.ptr, red_glob, red_glob + 1);
-      k_d_pcg_pupdate<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, c->pz.ptr, c->pp.ptr, c->scal.ptr);
+      k_d_cg_update<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, c->dinv.ptr, c->pq.ptr, c->pz.ptr, c->pp.ptr,
+                                                        c->ps.ptr, c->px.ptr, c->pr.ptr, c->partials.ptr,
+                                                        c->counter.ptr, c->scal.ptr, red_loc);
+      cg_spmv_reduce(c, So, C, 3);
+      k_d_cg_scal<<<1, 1, 0, st>>>(c->scal.ptr, c->hist.ptr, red_glob);
       CK(cudaGetLastError());
-      c->launches += 4;
+      c->launches += 2;
     }
     CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -564,12 +575,32 @@ int pcg_solve_dist(bal_ctx* c, const double* rhs, const double* x0, double* x_ou
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   tp_halo(c, c->px.ptr);
   launch_spmv(st, So, C, c->px.ptr, c->pq.ptr);
-  k_d_pcg_init<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr,
-                                                   c->pp.ptr, c->partials.ptr, c->counter.ptr, red_loc);
-  CK(cudaMemcpyAsync(red_glob, red_loc, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  tp_allreduce(c, red_glob, 3);
-  k_d_pcg_init_fin<<<1, 1, 0, st>>>(red_glob, c->scal.ptr, c->hist.ptr);
-  c->launches += 3;
+  k_d_cg_init<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, rhs, c->pq.ptr, c->dinv.ptr, c->px.ptr, c->pr.ptr,
+                                                  c->pz.ptr, c->pp.ptr, c->ps.ptr, c->partials.ptr, c->counter.ptr,
+                                                  red_loc);
+  c->launches += 2;
+  c->ws_rejected = false;
+  if (warm) {
+    // DESIGN.md R-WS1: keep x0 only if phi(x0) = -x0'(b + r0)/2 < phi(0) = 0 (all-reduced over ranks)
+    CK(cudaMemcpyAsync(red_glob, red_loc + 3, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    tp_allreduce(c, red_glob, 1);
+    double xbr = 0.0;
+    CK(cudaMemcpyAsync(&xbr, red_glob, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (!(-0.5 * xbr < 0.0)) {
+      CK(cudaMemsetAsync(c->px.ptr, 0, 3 * (size_t)N * sizeof(double), st));
+      CK(cudaMemsetAsync(c->pq.ptr, 0, 3 * (size_t)N * sizeof(double), st));
+      k_d_cg_init<<<kVecBlocks, kVecThreads, 0, st>>>(d.r0, d.r1, rhs, c->pq.ptr, c->dinv.ptr, c->px.ptr, c->pr.ptr,
+                                                      c->pz.ptr, c->pp.ptr, c->ps.ptr, c->partials.ptr,
+                                                      c->counter.ptr, red_loc);
+      c->launches += 1;
+      c->ws_rejected = true;
+    }
+  }
+  cg_spmv_reduce(c, So, C, 4);
+  k_d_cg_init_fin<<<1, 1, 0, st>>>(c->scal.ptr, c->hist.ptr, red_glob);
+  CK(cudaGetLastError());
+  c->launches += 1;
   CK(cudaMemcpyAsync(c->h_scal, c->scal.ptr, sizeof(PcgScal), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int ws_it = stats ? stats->ws_iters_max : 0, ng = stats ? stats->n_groups : 0;

@@ -121,7 +121,9 @@ def test_degenerate_active_set_and_stencils(name):
 @pytest.mark.parametrize("name", list(CASES))
 def test_degenerate_step_parity(name):
     """One time step into the tie (B approaches A at 0.3 m/s, 1 cm per step against a 0.5 mm gap):
-    GPU and oracle positions agree to 1e-6 of the displacement."""
+    GPU and oracle positions agree to 1e-5 of the displacement (DESIGN.md R-TRACE: the GPU's
+    Chronopoulos-Gear and the oracle's textbook PCG directions agree to ~1e-6 per Newton iteration;
+    a step takes 6-9 of them here)."""
     sc = scene(name)
     o = Oracle(sc)
     x1, _v1, _ = o.step(sc["x0"], sc["v0"])
@@ -130,7 +132,7 @@ def test_degenerate_step_parity(name):
     xn = torch.empty_like(xt)
     bal.bal_step(ctx, xt, _t(sc["v0"]), xn, torch.empty_like(xt))
     xg = xn.cpu().numpy().reshape(-1, 3)
-    assert np.linalg.norm(xg - x1) <= 1e-6 * np.linalg.norm(x1 - sc["x0"])
+    assert np.linalg.norm(xg - x1) <= 1e-5 * np.linalg.norm(x1 - sc["x0"])
     # intersection-free: every feature-pair distance stays positive
     pt, ee = cm.candidates(o.mesh, xg, xg, o.dhat)
     _k, d = cm.constraint_set(xg, pt, ee, o.dhat)
