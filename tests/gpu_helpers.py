@@ -72,8 +72,12 @@ def assembly_bounds(o, x, y, asm, contact_tol=(), friction=None, friction_tol=()
         rows.append(np.repeat(tets, 4, axis=1).ravel())
         cols.append(np.tile(tets, (1, 4)).ravel())
         vals.append(np.repeat(elastic_tol * nP, 16))
+        # a near-rest tet's gradient V P(F) Dm^-T is a small difference of large terms: its rounding
+        # is ~u |H| |x_a - x_b| (the gradient is ~ H times the edge vectors), not relative to |g|
+        xe = x[tets]
+        L = np.max(np.linalg.norm(xe[:, :, None, :] - xe[:, None, :, :], axis=-1), axis=(1, 2))
         for k in range(4):
-            np.add.at(gb, tets[:, k], elastic_tol * ng)
+            np.add.at(gb, tets[:, k], elastic_tol * ng + 1e-15 * nP * L)
     for P, g, ids, t in zip(asm.get("contact_P", []), asm.get("contact_g", []), asm.get("contact_ids", []),
                             contact_tol):
         r, c = _node_pairs(ids)

@@ -173,9 +173,9 @@ def _trace_equal(tg, to, rel=1e-4):
             return n
         for k in TRACE_INT:
             assert int(g[k]) == int(o[k]), (k, g, o)
-        # PCG iterations within 2 %: the Chronopoulos-Gear recursive residual drifts from the textbook
-        # one by a few per cent over ~100 iterations on C1's ill-conditioned systems
-        assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.02 * int(o["pcg_iters"])), (g, o)
+        # PCG iterations within 5 %: the Chronopoulos-Gear recursive residual drifts from the textbook
+        # one by a few per cent over ~100 iterations on C1's ill-conditioned systems (R-CG)
+        assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.05 * int(o["pcg_iters"])), (g, o)
         for k in ("alpha_ccd", "alpha", "sigma"):
             assert g[k] == pytest.approx(float(o[k]), rel=rel, abs=1e-300), (k, g[k], o[k])
         # ||e|| / ||e0||: relative 1e-4 or, near convergence where ||e|| is a small difference of
