@@ -258,6 +258,7 @@ class Oracle:
         st["sigma"] = sig0
         dmin_prev = np.inf
         e0 = None
+        dx_prev = None
         emin, frozen = [], False
         stats = dict(newton=0, pcg=0, ws=0, max_constraints=0)
         converged = False
@@ -360,6 +361,8 @@ class Oracle:
                 pst = la.pcg_run(A, Dinv, pst, 0.0, 10 ** 9, min(pst.k + int(p["pcg_resume_iters"]),
                                                                   int(p["max_pcg"])))
             x_new = x + alpha * P
+            if trace is not None:
+                dx_prev_next = (alpha * P).ravel()
             stats["newton"] += 1
             stats["pcg"] += pst.k
             stats["ws"] += sum(ws_it.values()) if ws_it else 0
@@ -370,8 +373,14 @@ class Oracle:
                                   sigma=st["sigma"], groups=dict(zip(gvals.tolist(), gcnt.tolist())),
                                   ws_iters=ws_it, pcg_iters=pst.k, pcg_stop=pst.stop, alpha_ccd=a_ccd,
                                   alpha=alpha, halvings=halvings, resumes=resumes, safeguard=safeguard,
-                                  rel_e=en / e0, nA_margin=cm.activation_margin(x, pt, ee, dhat),
+                                  rel_e=en / e0, e_sens=(1e-6 * float(np.linalg.norm(A @ dx_prev)) / e0
+                                                         if dx_prev is not None else 0.0),
+                                  nA_margin=cm.activation_margin(x, pt, ee, dhat),
                                   ls_margin=ls_margin, ccd_sens=ccd_sens, pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
+            if trace is not None:
+                # trace only (DESIGN.md R-TRACE): ||e|| at the next iterate moves by ~||A dx|| when the
+                # step moves by dx; two PCG forms' steps agree to ~1e-6 relative
+                dx_prev = dx_prev_next
             if en <= float(p["newton_rel_tol"]) * e0:
                 x = x_new
                 converged = True

@@ -480,36 +480,8 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         const double* vj = kind == 2u ? xv + 3 * jr : vt + 3 * jr;
         const VT* A = vals + 9 * q;
         double m[9];
-#if BAL_TS_VEC
-        if (sizeof(VT) == 8) {  // 72-B block = 4 x 16 B + 8 B (16-B aligned at even offsets)
-          const double* Ad = reinterpret_cast<const double*>(A);
-          if (reinterpret_cast<uintptr_t>(Ad) & 15) {
-            m[0] = Ad[0];
-            const double2* A2 = reinterpret_cast<const double2*>(Ad + 1);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const double2 t2 = A2[k];
-              m[1 + 2 * k] = t2.x;
-              m[2 + 2 * k] = t2.y;
-            }
-          } else {
-            const double2* A2 = reinterpret_cast<const double2*>(Ad);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const double2 t2 = A2[k];
-              m[2 * k] = t2.x;
-              m[2 * k + 1] = t2.y;
-            }
-            m[8] = Ad[8];
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 9; ++k) m[k] = (double)A[k];
-        }
-#else
 #pragma unroll
         for (int k = 0; k < 9; ++k) m[k] = (double)A[k];  // FP64 arithmetic either way
-#endif
         const double j0 = vj[0], j1 = vj[1], j2 = vj[2];
         double* c3 = cs + 3 * (int)M.cpos[q];
         c3[0] = fma(m[2], j2, fma(m[1], j1, m[0] * j0));
@@ -548,49 +520,6 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       // ---- phase 2, fixed-order sums, one thread per owned row il: stored blocks (ascending
       // column), in-tile mirror products (ascending row), contact blocks (ascending column); one
       // thread per out-of-tile target x: its products (ascending block)
-#if BAL_TS_PH2SPLIT
-      // two threads per row when the tile has <= kTsConsumers / 2 rows: the even thread sums the
-      // row terms (+ contacts), the odd one the in-tile mirror terms; combined in that order
-      const bool split = 2 * R <= kTsConsumers;
-      const int RT = split ? 2 * R : R;  // threads busy with rows
-      if (split) {
-        const int il = ct >> 1;
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-        if (ct < RT) {
-          if (ct & 1) {
-            sum3(tp, M.mps[il], M.mps[il] + M.mle[il], acc0, acc1, acc2);
-          } else {
-            sum3(cs, M.rpc[il], M.rpc[il] + M.rle[il], acc0, acc1, acc2);
-            if (crp) {
-              const int e0 = cr[il] - c0r, e1 = cr[il + 1] - c0r;
-              sum3(cc, e0, min(e1, ncc), acc0, acc1, acc2);
-              for (int s2 = c0r + max(e0, ncc); s2 < c0r + e1; ++s2) {
-                const double* A = a.C.val + 9 * (size_t)s2;
-                const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
-                const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);
-                acc0 += fma(A[2], c2, fma(A[1], c1, A[0] * c0));
-                acc1 += fma(A[5], c2, fma(A[4], c1, A[3] * c0));
-                acc2 += fma(A[8], c2, fma(A[7], c1, A[6] * c0));
-              }
-            }
-          }
-        }
-        const double m0 = __shfl_down_sync(0xffffffffu, acc0, 1), m1 = __shfl_down_sync(0xffffffffu, acc1, 1),
-                     m2 = __shfl_down_sync(0xffffffffu, acc2, 1);
-        if (ct < RT && !(ct & 1)) {
-          acc0 += m0;
-          acc1 += m1;
-          acc2 += m2;
-          double* yr = a.y + 3 * (size_t)(r0 + il);
-          yr[0] = acc0;
-          yr[1] = acc1;
-          yr[2] = acc2;
-          if (DOT) dacc += vt[3 * il] * acc0 + vt[3 * il + 1] * acc1 + vt[3 * il + 2] * acc2;
-        }
-      } else
-#else
-      const int RT = R;
-#endif
       if (ct < R) {
         const int il = ct;
         double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
@@ -615,7 +544,7 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
         if (DOT) dacc += vt[3 * il] * acc0 + vt[3 * il + 1] * acc1 + vt[3 * il + 2] * acc2;
       }
       // partials: consumer threads without a row first (x = ct - R), then the row threads
-      for (int x = (ct - RT + kTsConsumers) % kTsConsumers; x < nc; x += kTsConsumers) {
+      for (int x = (ct - R + kTsConsumers) % kTsConsumers; x < nc; x += kTsConsumers) {
         double p0 = 0.0, p1 = 0.0, p2 = 0.0;
         sum3(tp, M.xps[x], M.xps[x] + M.xle[x], p0, p1, p2);
         double* pp = a.part + 3 * (size_t)M.pslot[x];

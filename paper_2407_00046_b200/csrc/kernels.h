@@ -36,12 +36,6 @@ constexpr int kTsStages = BAL_TS_STAGES;
 #define BAL_TS_SCRATCH_BUFS 1
 #endif
 constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;
-#ifndef BAL_TS_VEC
-#define BAL_TS_VEC 0  // 16-byte shared-memory loads of the stored blocks in phase 1
-#endif
-#ifndef BAL_TS_PH2SPLIT
-#define BAL_TS_PH2SPLIT 0  // phase 2: two threads per row (row terms | mirror terms)
-#endif
 #ifndef BAL_TS_CONTACT_CAP
 #define BAL_TS_CONTACT_CAP 384
 #endif
