@@ -81,6 +81,12 @@ typedef struct { double E, nu, rho; } bal_material;
                               * stored static blocks rounded to FP32 (36 B instead of 72 B per block);
                               * arithmetic, vectors, contact blocks, preconditioner and warm start stay FP64 */
 
+#define BAL_ADDITIVE_PRECOND 512u /* NEXT-1 ablation (App. A, "comparison only"): the global PCG
+                                   * uses the two-level additive preconditioner M^-1 = D^-1 + sum over
+                                   * 9-node aggregates of B^T (B A B^T)^-1 B (27x27 Gauss-Jordan inverses
+                                   * once per Newton step; DESIGN.md R-AS1) instead of block-Jacobi D^-1;
+                                   * single-GPU tile-SpMV path only (else BAL_E_INVALID_ARG) */
+
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {
   double h;              /* time step (s) */

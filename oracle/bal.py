@@ -40,6 +40,8 @@ FLAG_SIGMA_MIN = 16  # min(1.2 sigma, 100 sigma0) reading of Alg. 1 line 16 (the
 FLAG_FRICTION_NO_FREEZE = 32  # literal per-iteration anchors (disables R-FRIC1)
 FLAG_CCD_LITERAL = 64  # literal P:468 CCD activation eps + dhat (disables R-CCD2; the GPU's BAL_CCD_LITERAL)
 FLAG_PCG_LITERAL_STALL = 128  # literal residual stagnation test (Q15; disables R-PCG1; BAL_PCG_LITERAL_STALL)
+FLAG_ADDITIVE_PRECOND = 512  # NEXT-1: global PCG with App. A's two-level additive preconditioner (R-AS1)
+AS_AGG_NODES = 9  # R-AS1: level-2 aggregates of 9 consecutive nodes (27x27 blocks)
 FREEZE_WINDOW = 10  # R-FRIC1 window (the GPU's kFreezeWindow)
 
 
@@ -315,7 +317,8 @@ class Oracle:
                 # the A-norm, i.e. phi(x0) = x0'A x0 / 2 - b'x0 < phi(0) = 0
                 if not (0.5 * float(x0 @ (A @ x0)) - float(b @ x0) < 0.0):
                     x0 = np.zeros_like(b)
-            pst = la.pcg(A, b, x0, Dinv, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
+            M = la.additive_schwarz(A, Dinv, AS_AGG_NODES) if self.flags & FLAG_ADDITIVE_PRECOND else Dinv
+            pst = la.pcg(A, b, x0, M, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
                          int(p["max_pcg"]), bool(self.flags & FLAG_PCG_LITERAL_STALL))
             resumes = 0
             while True:
@@ -358,7 +361,7 @@ class Oracle:
                 if resumes >= 50 or pst.k >= int(p["max_pcg"]):
                     raise NotConverged("line search failed after PCG resumes")
                 resumes += 1
-                pst = la.pcg_run(A, Dinv, pst, 0.0, 10 ** 9, min(pst.k + int(p["pcg_resume_iters"]),
+                pst = la.pcg_run(A, M, pst, 0.0, 10 ** 9, min(pst.k + int(p["pcg_resume_iters"]),
                                                                   int(p["max_pcg"])))
             x_new = x + alpha * P
             if trace is not None:

@@ -40,6 +40,38 @@ def apply_block(Dinv, r):
     return np.einsum("nij,nj->ni", Dinv, r.reshape(N, 3)).ravel()
 
 
+def precond(M, r):
+    """Apply the preconditioner: M is the block-Jacobi inverse (N,3,3) or, for the additive
+    preconditioner of App. A, a callable r -> M^-1 r."""
+    return M(r) if callable(M) else apply_block(M, r)
+
+
+def additive_schwarz(A, Dinv, agg_nodes=9):
+    """Two-level additive preconditioner of App. A ("comparison only, not
+    adopted"): M^-1 = sum_b B_b^T (B_b A B_b^T)^-1 B_b over
+      level 1: every node's 3x3 diagonal block (the block-Jacobi inverse Dinv), and
+      level 2: aggregates of `agg_nodes` consecutive nodes [a0, a0 + agg_nodes) (the last one ragged),
+               i.e. the 3 agg_nodes x 3 agg_nodes principal submatrices ("27x27" for 9 nodes),
+    each inverse precomputed once per Newton step (the library inverse stands in for the
+    paper's Gauss-Jordan elimination).  DESIGN.md R-AS1 states the reading.  Returns a callable."""
+    N = A.shape[0] // 3
+    A = A.tocsr()
+    blocks = []
+    for a0 in range(0, N, agg_nodes):
+        a1 = min(a0 + agg_nodes, N)
+        idx = np.arange(3 * a0, 3 * a1)
+        blocks.append((3 * a0, 3 * a1, np.linalg.inv(A[idx][:, idx].toarray())))
+
+    def apply(r):
+        z = apply_block(Dinv, r)
+        for i0, i1, Binv in blocks:
+            z[i0:i1] += Binv @ r[i0:i1]
+        return z
+
+    apply.blocks = blocks
+    return apply
+
+
 class PCGState:
     """Saved PCG state so App. B's 'return to PCG for an additional 100 iterations' can resume."""
 
@@ -54,7 +86,7 @@ class PCGState:
 
 def pcg_start(A, b, x0, Dinv):
     r = b - A @ x0
-    z = apply_block(Dinv, r)
+    z = precond(Dinv, r)
     return PCGState(x0.copy(), r, z, z.copy(), float(r @ z), [float(np.linalg.norm(r))],
                     float(np.linalg.norm(b)))
 
@@ -94,7 +126,7 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters, literal_stall=False):
         st.dec.append(st.dec[-1] + 0.5 * alpha * st.rz)  # phi(x + a p) = phi(x) - a rho / 2
         st.x = st.x + alpha * st.p
         st.r = st.r - alpha * q
-        st.z = apply_block(Dinv, st.r)
+        st.z = precond(Dinv, st.r)
         rz_new = float(st.r @ st.z)
         beta = rz_new / st.rz if st.rz != 0.0 else 0.0  # r = 0 exactly: converged, next check stops
         st.rz = rz_new
@@ -132,7 +164,7 @@ def cg_start(A, b, x0, Dinv):
         alpha_{k+1} = gam_{k+1} / (delta_{k+1} - beta_{k+1} gam_{k+1} / alpha_k)."""
     x = x0.copy()
     r = b - A @ x
-    u = apply_block(Dinv, r)
+    u = precond(Dinv, r)
     st = CGState(x, r, u, np.zeros_like(b), float(r @ u), [float(np.linalg.norm(r))], float(np.linalg.norm(b)))
     st.u, st.w, st.s = u, A @ u, np.zeros_like(b)
     delta = float(st.w @ u)
@@ -163,7 +195,7 @@ def cg_run(A, Dinv, st, tol, window, max_iters, literal_stall=False):
         st.s = st.w + st.beta * st.s
         st.x = st.x + st.alpha * st.p
         st.r = st.r - st.alpha * st.s
-        st.u = apply_block(Dinv, st.r)
+        st.u = precond(Dinv, st.r)
         st.w = A @ st.u
         gam_new = float(st.r @ st.u)
         delta = float(st.w @ st.u)

@@ -32,6 +32,7 @@ BAL_FRICTION_NO_FREEZE = 32
 BAL_CCD_LITERAL = 64
 BAL_PCG_LITERAL_STALL = 128
 BAL_FP32_MATRIX = 256
+BAL_ADDITIVE_PRECOND = 512
 
 
 class bal_mesh(C.Structure):

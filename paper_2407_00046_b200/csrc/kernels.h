@@ -42,6 +42,9 @@ constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;
 constexpr int kTsContactCap = BAL_TS_CONTACT_CAP;  // contact blocks per tile computed block-parallel  // 2: consecutive tiles' scratch double-buffered
 constexpr int kTsMaxRows = kTsConsumers;  // one consumer thread per owned row
 
+// NEXT-1 additive preconditioner (k_additive.cu, App. A): level-2 aggregate size in nodes (27x27)
+constexpr int kAsAggNodes = 9;
+
 constexpr int kElasticThreads = 128;
 constexpr int kMaxGroups = 64;
 
@@ -123,6 +126,13 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
 // w_own = A u (+ partials) with the fused single-reduction PCG epilogue (cg_scalars)
 void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const double* u, double* w, double* part,
                         double* dpart, unsigned* counter, PcgScal* sc, const double* upart, double* hist);
+// App. A additive preconditioner (k_additive.cu): level-2 inverses of 9-node aggregates from the full
+// static BSR + contact BSR (bad = 1 if a pivot is not positive); u += A_agg^-1 r, upart[2b] += (r, .)
+int as_num_aggregates(int N);
+void launch_as_build(cudaStream_t st, int N, const int* srp, const int* scol, const double* sval, const int* crp,
+                     const int* ccol, const double* cval, double* inv, int* bad);
+void launch_as_apply(cudaStream_t st, int N, const double* inv, const double* r, double* u, double* upart,
+                     const PcgScal* sc);
 // Chronopoulos-Gear PCG (k_linalg.cu): init from A x0 (complete) and the per-iteration update
 void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
                     double* u, double* p, double* s, double* upart, double* partials, unsigned* counter,

@@ -56,6 +56,28 @@ void compact_groups(bal_ctx* c) {
   c->launches += 2;
 }
 
+// NEXT-1 (App. A, R-AS1): level-2 inverses of the current system, once per solve (= once per Newton
+// iteration; App. B resumes reuse them)
+static void as_build(bal_ctx* c) {
+  cudaStream_t st = c->st;
+  const int N = c->N;
+  c->as_inv.reserve((size_t)as_num_aggregates(N) * 9 * kAsAggNodes * kAsAggNodes + 1);
+  const int* srp = c->loaded_bsr ? c->lb_row_ptr.ptr : c->sp.row_ptr;
+  const int* scol = c->loaded_bsr ? c->lb_col.ptr : c->sp.col;
+  const double* sval = c->loaded_bsr ? c->lb_val.ptr : c->sval.ptr;
+  const Bsr C = c->contact_bsr();
+  c->tmp_i.reserve(2);
+  CK(cudaMemsetAsync(c->tmp_i.ptr, 0, sizeof(int), st));
+  launch_as_build(st, N, srp, scol, sval, C.nnzb ? C.row_ptr : nullptr, C.col, C.val, c->as_inv.ptr, c->tmp_i.ptr);
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->tmp_i.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  c->launches += 1;
+  if (bad) throw std::invalid_argument("BAL_ADDITIVE_PRECOND: an aggregate block is not positive definite");
+}
+
+static bool as_on(const bal_ctx* c) { return (c->prm.flags & BAL_ADDITIVE_PRECOND) != 0; }
+
 // One batch = kBatch PCG iterations (SpMV+dot, update, p-update) + a D2H copy of the scalars and a
 // completion event, captured once per solve into a CUDA graph.  Two graphs (ping-pong event sets
 // and host buffers) keep one batch queued while the host inspects the previous one, so the GPU never
@@ -80,6 +102,7 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
       // grid-wide reduction, App. B stop test, alpha / beta)
       launch_cg_update(st, N, c->dinv.ptr, S.ts->pin_ptr, S.ts->part, c->pq.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr,
                        c->px.ptr, c->pr.ptr, c->upart.ptr, c->scal.ptr);
+      if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, c->scal.ptr);
       if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
       launch_spmv_ts_dot(st, S, C, c->pz.ptr, c->pq.ptr, S.ts->part, c->dpart.ptr, c->counter.ptr, c->scal.ptr,
                          c->upart.ptr, c->hist.ptr);
@@ -117,7 +140,7 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
   int k_prev = c->h_scal->k;
   CK(cudaGraphLaunch(ge[0], st));
   CK(cudaGraphLaunch(ge[1], st));
-  const int per_iter = (ts_usable(S) || pcg_fused_grid(c->N) > 0) ? 2 : 3;
+  const int per_iter = (ts_usable(S) || pcg_fused_grid(c->N) > 0) ? 2 + (as_on(c) ? 1 : 0) : 3;
   c->launches += 2 * per_iter * kBatch;
   int cur = 0;
   while (true) {
@@ -244,11 +267,17 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.pmin = INFINITY;
   h.stall_rel = stall_rel();
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  if (as_on(c)) {
+    if (!ts_usable(S))
+      throw std::invalid_argument("BAL_ADDITIVE_PRECOND needs the single-GPU tile-SpMV (Chronopoulos-Gear) path");
+    as_build(c);
+  }
   launch_spmv(st, S, C, c->px.ptr, c->pq.ptr);
   if (ts_usable(S)) {
     // single-reduction (Chronopoulos-Gear) PCG: init, then SpMV 0 (w_0 = A u_0, stop test at k = 0)
     launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
                    c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+    if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, nullptr);
     if (warm && ws_guard_rejects(c, rhs)) {
       // DESIGN.md R-WS1: the warm start is used only when it is closer to the solution than x = 0 in the
       // A-norm, phi(x0) = x0'A x0 / 2 - b'x0 < phi(0) = 0; else the solve starts from 0
@@ -256,6 +285,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
       CK(cudaMemsetAsync(c->pq.ptr, 0, 3 * (size_t)N * sizeof(double), st));
       launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
                      c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+      if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, nullptr);
       c->launches += 1;
       c->ws_rejected = true;
     }

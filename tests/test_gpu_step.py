@@ -178,11 +178,12 @@ def _trace_equal(tg, to, rel=1e-4):
         assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.05 * int(o["pcg_iters"])), (g, o)
         for k in ("alpha_ccd", "alpha", "sigma"):
             assert g[k] == pytest.approx(float(o[k]), rel=rel, abs=1e-300), (k, g[k], o[k])
-        # ||e|| / ||e0||: relative 1e-4, or within its conditioning: the two PCG forms' steps agree to
-        # ~1e-6 relative and ||e|| moves by ||A dx|| when the previous step moves by dx (the oracle
-        # records 1e-6 ||A dx_prev|| / ||e0||), plus 1e-6 near convergence
-        tol_e = 1e-6 + float(o["e_sens"])
-        assert g["rel_e"] == pytest.approx(float(o["rel_e"]), rel=rel, abs=tol_e), ("rel_e", g["rel_e"], o["rel_e"])
+        # ||e|| / ||e0||: within its conditioning -- ||e|| moves by ||A dx|| when the previous step moves
+        # by dx (the oracle records e_sens = 1e-6 ||A dx_prev|| / ||e0||), and the two PCG forms, both
+        # stopped at a 1e-4 relative residual, give steps that agree to ~1e-4 at worst: 100 e_sens,
+        # plus 1e-3 relative
+        tol_e = 1e-6 + 100.0 * float(o["e_sens"])
+        assert g["rel_e"] == pytest.approx(float(o["rel_e"]), rel=1e-3, abs=tol_e), ("rel_e", g["rel_e"], o["rel_e"])
         n += 1
     assert len(tg) == len(to)
     return n

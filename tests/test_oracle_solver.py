@@ -214,3 +214,55 @@ def test_warm_start_exact_on_decoupled_groups():
     assert st.k <= 1
     x0z, _ = la.warm_start(A, np.zeros(42), groups, Dinv, np.zeros(14, bool))
     assert np.all(x0z == 0)
+
+
+def test_additive_schwarz_is_the_printed_sum_and_its_special_cases():
+    """App. A two-level additive preconditioner, DESIGN.md R-AS1.
+    (1) apply(r) equals the printed M^-1 = sum_i B_i^T (B_i A B_i^T)^-1 B_i with explicit 0/1
+        block-mapping matrices B_i (3x3 node blocks + 9-node aggregates, a ragged last one);
+    (2) A with no coupling between nodes: the aggregate inverses are blockdiag(D_j^-1), so
+        M^-1 = 2 A^-1 and PCG from 0 lands on A^-1 b after ONE iteration (alpha = 1/2);
+    (3) symmetric positive definite on a C1 system; (4) Chronopoulos-Gear == textbook iterates with it."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(31)
+    bs = _rand_spd_blocks(rng, 22, cond_scale=1e2)  # 22 nodes: aggregates 9, 9, 4
+    A = bs.to_csr()
+    Dinv = np.linalg.inv(bs.diag_blocks())
+    M = la.additive_schwarz(A, Dinv, 9)
+    n = A.shape[0]
+    Ad = A.toarray()
+    Mi = np.zeros((n, n))
+    sets = [[j] for j in range(22)] + [list(range(0, 9)), list(range(9, 18)), list(range(18, 22))]
+    for nodes in sets:
+        B = np.zeros((3 * len(nodes), n))
+        for a, j in enumerate(nodes):
+            B[3 * a:3 * a + 3, 3 * j:3 * j + 3] = np.eye(3)
+        Mi += B.T @ np.linalg.inv(B @ Ad @ B.T) @ B
+    for _ in range(3):
+        r = rng.normal(size=n)
+        assert np.linalg.norm(M(r) - Mi @ r) <= 1e-12 * np.linalg.norm(Mi @ r)
+    # (2) decoupled nodes
+    blocks = np.stack([np.eye(3) * (1.0 + j) + 0.1 * np.ones((3, 3)) for j in range(12)])
+    Ab = sp.block_diag(list(blocks)).tocsr()
+    Db = np.linalg.inv(blocks)
+    b = rng.normal(size=36)
+    st = la.pcg(Ab, b, np.zeros(36), la.additive_schwarz(Ab, Db, 9), tol=1e-13, window=10 ** 9)
+    assert st.k == 1
+    assert np.linalg.norm(st.x - np.linalg.solve(Ab.toarray(), b)) <= 1e-13 * np.linalg.norm(st.x)
+    # (3) SPD on a C1 system (436 nodes: 48 aggregates of 9 + one of 4)
+    sc = scenes.make_cubes(1)
+    o = Oracle(sc)
+    x = sc["x0"]
+    st0 = dict(y=x.copy(), x_t=x.copy(), sigma=1.0, ap_keys=np.zeros((0, 5), np.int64), ap_mu=np.zeros(0),
+               ap_s=np.zeros(0), fr_keys=None)
+    asm = o.assemble(x, st0, np.zeros((0, 5), np.int64))
+    Mc = la.additive_schwarz(asm["A"], asm["Dinv"], 9)
+    Md = np.stack([Mc(e) for e in np.eye(asm["A"].shape[0])[:120]], axis=1)  # first 40 nodes' columns
+    assert np.allclose(Md[:120], Md[:120].T, rtol=0, atol=1e-12 * np.abs(Md).max())
+    assert np.linalg.eigvalsh(0.5 * (Md[:120] + Md[:120].T)).min() > 0
+    # (4) both PCG forms with the additive preconditioner
+    b = rng.normal(size=n)
+    for k in (1, 5, 20):
+        a = la.pcg_cg(A, b, np.zeros(n), M, tol=0.0, window=10 ** 9, max_iters=k)
+        t = la.pcg(A, b, np.zeros(n), M, tol=0.0, window=10 ** 9, max_iters=k)
+        assert np.linalg.norm(a.x - t.x) <= 1e-10 * np.linalg.norm(t.x)

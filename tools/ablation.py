@@ -1,6 +1,7 @@
 """NEXT-1 ablations on the same kernels: warm start on/off (Fig. warm
 start), BAL vs plain inexact-Newton IPC (A' = empty, sigma = sigma^0), the capped and the
-min readings of the sigma schedule (Alg. 1 line 16).  Runs whole frames of a scene through
+min readings of the sigma schedule (Alg. 1 line 16), the two-level additive preconditioner of
+App. A alone and with the warm start.  Runs whole frames of a scene through
 bal_frame_* with each flag set and prints per-variant totals as JSON lines.
 
     python tools/ablation.py c1|c2|c3 [frames]      # whole frames
@@ -18,7 +19,9 @@ import scenes  # noqa: E402
 
 VARIANTS = {"bal+warmstart": 0, "bal, no warm start": bal.BAL_NO_WARMSTART,
             "inexact Newton (no AL)": bal.BAL_NO_AUGLAG, "sigma cap 1e8 sigma0": bal.BAL_SIGMA_CAP,
-            "sigma min(1.2 sigma, 100 sigma0)": bal.BAL_SIGMA_MIN}
+            "sigma min(1.2 sigma, 100 sigma0)": bal.BAL_SIGMA_MIN,
+            "additive precond (App. A) alone": bal.BAL_ADDITIVE_PRECOND | bal.BAL_NO_WARMSTART,
+            "additive precond + warm start": bal.BAL_ADDITIVE_PRECOND}
 
 
 def run(sc, flags, frames=None, newton=None):
