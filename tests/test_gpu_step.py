@@ -13,7 +13,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 import paper_2407_00046_b200 as bal  # noqa: E402
 from oracle import contact as cm  # noqa: E402
-from oracle.bal import Oracle  # noqa: E402
+from oracle.bal import FLAG_PCG_CG, Oracle  # noqa: E402
 from oracle.energy import nh_min_J  # noqa: E402
 
 DEV = torch.device("cuda:0")
@@ -173,9 +173,10 @@ def _trace_equal(tg, to, rel=1e-4):
             return n
         for k in TRACE_INT:
             assert int(g[k]) == int(o[k]), (k, g, o)
-        # PCG iterations within 5 %: the Chronopoulos-Gear recursive residual drifts from the textbook
-        # one by a few per cent over ~100 iterations on C1's ill-conditioned systems (R-CG)
-        assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.05 * int(o["pcg_iters"])), (g, o)
+        # PCG iterations within max(1, 2 %): the oracle runs the GPU's Chronopoulos-Gear form here
+        # (FLAG_PCG_CG; its textbook form drifts from it by up to ~6 % at ~100 iterations, R-CG); what
+        # remains is rounding of the same recurrences summed in another order
+        assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.02 * int(o["pcg_iters"])), (g, o)
         for k in ("alpha_ccd", "alpha", "sigma"):
             assert g[k] == pytest.approx(float(o[k]), rel=rel, abs=1e-300), (k, g[k], o[k])
         # ||e|| / ||e0||: within its conditioning -- ||e|| moves by ||A dx|| when the previous step moves
@@ -195,7 +196,7 @@ def test_cubes_decision_trace_equality():
     sigma, ||e||/||e0|| to 1e-6)."""
     sc = scenes.make_cubes(1)
     _xg, tg, _ = gpu_steps(sc, 10)
-    _xo, to = oracle_steps(sc, 10)
+    _xo, to = oracle_steps(sc, 10, flags=FLAG_PCG_CG)
     compared = sum(_trace_equal(tg[k], to[k]) for k in range(10))
     assert compared >= 0.5 * sum(len(t) for t in to), compared
 
@@ -209,7 +210,7 @@ def test_incline_friction_on_gpu(ratio):
     sc = scenes.make_incline(0, ratio=ratio, chi=chi)
     n = 8 if ratio < 1 else 6  # as the oracle pins (tests/test_oracle_friction.py)
     xg, tg, _ = gpu_steps(sc, n)
-    xo, to = oracle_steps(sc, n)
+    xo, to = oracle_steps(sc, n, flags=FLAG_PCG_CG)
     compared = 0
     for k in range(n):
         assert _rel(xg[k], xo[k], xo[k] - sc["x0"]) <= 1e-6, k
