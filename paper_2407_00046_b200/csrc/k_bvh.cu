@@ -62,17 +62,21 @@ __global__ void k_bounds(int n, const double* lo, const double* hi, double* part
     }
   }
 }
-__global__ void k_bounds_finish(int np, const double* part, double* out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(kRedThreads) k_bounds_finish(int np, const double* part, double* out) {
+  __shared__ double sh[kRedThreads / 32];
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int b = 0; b < np; ++b)
+  for (int b = threadIdx.x; b < np; b += blockDim.x)
     for (int c = 0; c < 3; ++c) {
       mn[c] = fmin(mn[c], part[6 * b + c]);
       mx[c] = fmax(mx[c], part[6 * b + 3 + c]);
     }
   for (int c = 0; c < 3; ++c) {
-    out[c] = mn[c];
-    out[3 + c] = mx[c];
+    const double a = block_min<kRedThreads>(mn[c], sh);
+    const double z = -block_min<kRedThreads>(-mx[c], sh);
+    if (threadIdx.x == 0) {
+      out[c] = a;
+      out[3 + c] = z;
+    }
   }
 }
 
@@ -183,7 +187,7 @@ void Lbvh::build(cudaStream_t st, int n_, int kind, const int* prims, const doub
   part.reserve(6 * kRedBlocks + 6);
   k_prim_boxes<<<ceil_div(n, 256), 256, 0, st>>>(n, kind, prims, xa, xb, h, lo.ptr, hi.ptr);
   k_bounds<<<kRedBlocks, kRedThreads, 0, st>>>(n, lo.ptr, hi.ptr, part.ptr);
-  k_bounds_finish<<<1, 32, 0, st>>>(kRedBlocks, part.ptr, part.ptr + 6 * kRedBlocks);
+  k_bounds_finish<<<1, kRedThreads, 0, st>>>(kRedBlocks, part.ptr, part.ptr + 6 * kRedBlocks);
   k_morton<<<ceil_div(n, 256), 256, 0, st>>>(n, lo.ptr, hi.ptr, part.ptr + 6 * kRedBlocks, keys.ptr);
   size_t t = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, t, keys.ptr, keys2.ptr, n, 0, 64, st));

@@ -21,7 +21,8 @@ VARIANTS = {"bal+warmstart": 0, "bal, no warm start": bal.BAL_NO_WARMSTART,
             "inexact Newton (no AL)": bal.BAL_NO_AUGLAG, "sigma cap 1e8 sigma0": bal.BAL_SIGMA_CAP,
             "sigma min(1.2 sigma, 100 sigma0)": bal.BAL_SIGMA_MIN,
             "additive precond (App. A) alone": bal.BAL_ADDITIVE_PRECOND | bal.BAL_NO_WARMSTART,
-            "additive precond + warm start": bal.BAL_ADDITIVE_PRECOND}
+            "additive precond + warm start": bal.BAL_ADDITIVE_PRECOND,
+            "fp32 matrix storage (NEXT-3)": bal.BAL_FP32_MATRIX}
 
 
 def run(sc, flags, frames=None, newton=None):

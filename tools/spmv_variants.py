@@ -18,7 +18,7 @@ sc = scenes.make_puffer_net(seed=4, settled=(cfg == "c4"))
 dev = torch.device("cuda:0")
 prm = dict(sc["params"])
 prm["max_pcg"] = 200
-ctx = bal.bal_init(sc, params=prm)
+ctx = bal.bal_init(sc, params=prm, flags=int(os.environ.get("BAL_FLAGS", "0")))
 x = torch.as_tensor(sc["x0"].ravel(), device=dev)
 v = torch.as_tensor(sc["v0"].ravel(), device=dev)
 bal.bal_frame_begin(ctx, x, v)
