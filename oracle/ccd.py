@@ -167,10 +167,27 @@ def pair_toi(ftype, x, dx, ids, dhat, d0frac=1e-2):
     return 1.0
 
 
-def step_toi(x, dx, pt, ee, dhat, d0frac=1e-2):
+def far_pairs(ftype, x, dx, pairs, dhat, d0frac=1e-2):
+    """Broad-phase refinement (result-neutral; DESIGN.md R-CCD4): pairs for which pair_toi returns 1.
+    The feature distance moves by at most ma + mb over the step (ma, mb = the largest displacement of
+    a vertex of either primitive: every point of a primitive is a convex combination of its vertices),
+    so if d(0) > ma + mb + 2 thr no root t in [0, 1] has d(t) < thr (2 thr + 1e-9 absorbs the rounding
+    of the computed distances); if also 0.9 d(0) >= ma + mb the identically-zero-cubic branch returns
+    min(1, 0.9 d(0) / (ma + mb)) = 1 as well."""
+    D0 = np.sqrt(resolve_features(x, ftype, pairs)[0])
+    na = 1 if ftype == PT else 2
+    disp = np.linalg.norm(dx[pairs], axis=2)
+    m = disp[:, :na].max(axis=1) + disp[:, na:].max(axis=1)
+    thr = EPS + np.minimum(dhat, d0frac * D0)
+    return (D0 > m + 2.0 * thr + 1e-9) & (0.9 * D0 >= m)
+
+
+def step_toi(x, dx, pt, ee, dhat, d0frac=1e-2, prefilter=True):
     """alpha_CCD = min over candidate pairs of the conservative TOI (1.0 if none)."""
     tmin = 1.0
     for ftype, pairs in ((PT, pt), (EE, ee)):
+        if prefilter and len(pairs):
+            pairs = pairs[~far_pairs(ftype, x, dx, pairs, dhat, d0frac)]
         for ids in pairs:
             t = pair_toi(ftype, x, dx, ids, dhat, d0frac)
             if t < tmin:

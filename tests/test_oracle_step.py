@@ -233,3 +233,33 @@ def test_literal_residual_stagnation_stops_with_a_useless_direction():
     assert obj.stop == la.STOP_CAP  # the objective kept decreasing: no stagnation stop
     phi = lambda x: 0.5 * x @ (A @ x) - b @ x  # noqa: E731
     assert phi(obj.x) < phi(lit.x) < 0.0
+
+
+def test_ccd_prefilter_is_result_neutral():
+    """DESIGN.md R-CCD4: pairs far_pairs() drops are exactly pairs whose pair_toi is 1 -- on random
+    pairs at every scale of distance vs displacement (far, grazing, colliding, in-plane motion),
+    and step_toi with and without the prefilter agree bitwise."""
+    rng = np.random.default_rng(37)
+    dropped = 0
+    for trial in range(600):
+        ftype = cm.PT if trial % 2 == 0 else cm.EE
+        x = rng.normal(size=(4, 3)) * 10.0 ** rng.uniform(-3, 0)
+        dx = rng.normal(size=(4, 3)) * 10.0 ** rng.uniform(-4, 0)
+        if trial % 7 == 0:
+            x[:, 2] = 0.0
+            dx[:, 2] = 0.0  # coplanar, in-plane motion: the identically-zero cubic
+        ids = np.array([[0, 1, 2, 3]])
+        D0, _, _ = cm.resolve_features(x, ftype, ids)
+        if np.sqrt(D0[0]) < 1e-9:
+            continue
+        far = ccd.far_pairs(ftype, x, dx, ids, 1e-3)[0]
+        if far:
+            dropped += 1
+            assert ccd.pair_toi(ftype, x, dx, ids[0], 1e-3) == 1.0
+    assert dropped > 50
+    sc = scenes.make_cubes(1)
+    o = Oracle(sc)
+    x1, _v, _ = o.step(sc["x0"], sc["v0"])
+    dx = 0.004 * rng.normal(size=x1.shape) * (~o.mesh.fixed[:, None])
+    pt, ee = cm.candidates(o.mesh, x1, x1 + dx, o.dhat)
+    assert ccd.step_toi(x1, dx, pt, ee, o.dhat) == ccd.step_toi(x1, dx, pt, ee, o.dhat, prefilter=False)
