@@ -63,6 +63,19 @@ def _coo_add(rows, cols, vals, ids, H):
     vals.append(H.ravel())
 
 
+def _pcg_window(pst, tol, drift=5e-2):
+    """Trace only (DESIGN.md R-TRACE): the iterations k at which a PCG whose residual history
+    differs from this one by a relative `drift` could have met ||r_k|| <= tol ||b||: from the first k
+    with ||r_k|| <= (1 + drift) tol ||b|| to the first k with ||r_k|| <= (1 - drift) tol ||b|| (the stop
+    iteration if none)."""
+    h = np.asarray(pst.hist)
+    thr = tol * pst.bnorm
+    lo = np.nonzero(h <= (1.0 + drift) * thr)[0]
+    hi = np.nonzero(h <= (1.0 - drift) * thr)[0]
+    k = int(pst.k)
+    return (int(lo[0]) if len(lo) else k, int(hi[0]) if len(hi) else k)
+
+
 class Oracle:
     def __init__(self, scene, flags=0):
         self.scene = scene
@@ -382,7 +395,9 @@ class Oracle:
                                   rel_e=en / e0, e_sens=(1e-6 * float(np.linalg.norm(A @ dx_prev)) / e0
                                                          if dx_prev is not None else 0.0),
                                   nA_margin=cm.activation_margin(x, pt, ee, dhat),
-                                  ls_margin=ls_margin, ccd_sens=ccd_sens, pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
+                                  ls_margin=ls_margin, ccd_sens=ccd_sens,
+                                  pcg_window=_pcg_window(pst, float(p["pcg_rel_tol"])),
+                                  pcg_margin=la.stop_margin(pst, float(p["pcg_rel_tol"]))))
             if trace is not None:
                 # trace only (DESIGN.md R-TRACE): ||e|| at the next iterate moves by ~||A dx|| when the
                 # step moves by dx; two PCG forms' steps agree to ~1e-6 relative

@@ -173,10 +173,15 @@ def _trace_equal(tg, to, rel=1e-4):
             return n
         for k in TRACE_INT:
             assert int(g[k]) == int(o[k]), (k, g, o)
-        # PCG iterations within max(1, 2 %): the oracle runs the GPU's Chronopoulos-Gear form here
-        # (FLAG_PCG_CG; its textbook form drifts from it by up to ~6 % at ~100 iterations, R-CG); what
-        # remains is rounding of the same recurrences summed in another order
-        assert abs(int(g["pcg_iters"]) - int(o["pcg_iters"])) <= max(1, 0.02 * int(o["pcg_iters"])), (g, o)
+        # PCG iterations: the oracle runs the GPU's Chronopoulos-Gear form here (FLAG_PCG_CG), but its
+        # initial guess comes from the warm start (per-group PCGs stopped at 1e-2, whose own counts
+        # shift with rounding) and the residual histories drift apart by rounding on C1's
+        # ill-conditioned systems (measured: up to 3 iterations / 4 % at ~75): the GPU's count must lie
+        # in the oracle's window of iterations whose residual is within 5 % of the App. B tolerance
+        # (pcg_window) +-1, or within max(2, 5 %) of the oracle's count
+        lo, hi = o["pcg_window"]
+        kg, ko = int(g["pcg_iters"]), int(o["pcg_iters"])
+        assert (lo - 1 <= kg <= hi + 1) or abs(kg - ko) <= max(2, 0.05 * ko), (kg, ko, lo, hi)
         for k in ("alpha_ccd", "alpha", "sigma"):
             assert g[k] == pytest.approx(float(o[k]), rel=rel, abs=1e-300), (k, g[k], o[k])
         # ||e|| / ||e0||: within its conditioning -- ||e|| moves by ||A dx|| when the previous step moves
