@@ -87,6 +87,14 @@ typedef struct { double E, nu, rho; } bal_material;
                                    * once per Newton step; DESIGN.md R-AS1) instead of block-Jacobi D^-1;
                                    * single-GPU tile-SpMV path only (else BAL_E_INVALID_ARG) */
 
+#define BAL_PCG_CRIT_I 1024u  /* NEXT-4 ablation, App. B criterion (i), truncated Newton: stop the global
+                               * PCG at ||r|| <= min(0.5, sqrt(||grad E||)) ||grad E|| (b = -grad E) */
+#define BAL_PCG_CRIT_II 2048u /* App. B criterion (ii): ||r_k|| <= u kappa(A) ||x_k|| (u = DBL_EPSILON, kappa from the
+                               * assembled eigenvalues: max e_j / min e_j over free nodes, DESIGN.md R-KAPPA) */
+#define BAL_PCG_CRIT_III 4096u /* App. B criterion (iii): ||r_k|| <= u kappa(A) ||b||.  (i)-(iii) replace only the
+                                * relative-residual test; stagnation (R-PCG1), cap and resumes are unchanged;
+                                * single-GPU tile-SpMV path only */
+
 /* Scene / solver parameters: Table 1 columns and the constants of Alg. 1 / App. B. */
 typedef struct {
   double h;              /* time step (s) */

@@ -41,8 +41,11 @@ FLAG_FRICTION_NO_FREEZE = 32  # literal per-iteration anchors (disables R-FRIC1)
 FLAG_CCD_LITERAL = 64  # literal P:468 CCD activation eps + dhat (disables R-CCD2; the GPU's BAL_CCD_LITERAL)
 FLAG_PCG_LITERAL_STALL = 128  # literal residual stagnation test (Q15; disables R-PCG1; BAL_PCG_LITERAL_STALL)
 FLAG_ADDITIVE_PRECOND = 512  # NEXT-1: global PCG with App. A's two-level additive preconditioner (R-AS1)
-FLAG_PCG_CG = 1024  # oracle only: global PCG in the Chronopoulos-Gear form (la.pcg_cg, pinned to the
+FLAG_PCG_CG = 1 << 20  # oracle only: global PCG in the Chronopoulos-Gear form (la.pcg_cg, pinned to the
 # textbook iterates) -- the GPU's form, for decision-trace parity of PCG iteration counts (R-CG)
+FLAG_PCG_CRIT_I = 1024  # NEXT-4: App. B criterion (i) (the GPU's BAL_PCG_CRIT_I)
+FLAG_PCG_CRIT_II = 2048  # App. B criterion (ii) (BAL_PCG_CRIT_II)
+FLAG_PCG_CRIT_III = 4096  # App. B criterion (iii) (BAL_PCG_CRIT_III)
 AS_AGG_NODES = 9  # R-AS1: level-2 aggregates of 9 consecutive nodes (27x27 blocks)
 FREEZE_WINDOW = 10  # R-FRIC1 window (the GPU's kFreezeWindow)
 
@@ -334,8 +337,15 @@ class Oracle:
                     x0 = np.zeros_like(b)
             M = la.additive_schwarz(A, Dinv, AS_AGG_NODES) if self.flags & FLAG_ADDITIVE_PRECOND else Dinv
             solve = la.pcg_cg if self.flags & FLAG_PCG_CG else la.pcg
+            crit = None
+            if self.flags & (FLAG_PCG_CRIT_I | FLAG_PCG_CRIT_II | FLAG_PCG_CRIT_III):
+                # App. B alternatives; kappa from the assembled eigenvalues (DESIGN.md R-KAPPA)
+                ej = asm["e_j"][self.free]
+                ukappa = np.finfo(np.float64).eps * float(ej.max() / ej.min())
+                crit = ("i" if self.flags & FLAG_PCG_CRIT_I else "ii" if self.flags & FLAG_PCG_CRIT_II else "iii",
+                        ukappa)
             pst = solve(A, b, x0, M, float(p["pcg_rel_tol"]), int(p["pcg_stall_window"]),
-                         int(p["max_pcg"]), bool(self.flags & FLAG_PCG_LITERAL_STALL))
+                        int(p["max_pcg"]), bool(self.flags & FLAG_PCG_LITERAL_STALL), crit=crit)
             resumes = 0
             while True:
                 dirn = pst.x.copy()
@@ -377,6 +387,7 @@ class Oracle:
                 if resumes >= 50 or pst.k >= int(p["max_pcg"]):
                     raise NotConverged("line search failed after PCG resumes")
                 resumes += 1
+                pst.crit = None  # App. B resume: exactly pcg_resume_iters more iterations
                 pst = (la.cg_run if self.flags & FLAG_PCG_CG else la.pcg_run)(A, M, pst, 0.0, 10 ** 9, min(pst.k + int(p["pcg_resume_iters"]),
                                                                   int(p["max_pcg"])))
             x_new = x + alpha * P

@@ -72,6 +72,21 @@ def additive_schwarz(A, Dinv, agg_nodes=9):
     return apply
 
 
+def stop_threshold(st, tol):
+    """||r_k|| threshold of the stop test: App. B's tol ||b|| (Q14), or one of App. B's alternatives
+    (P:753) when st.crit = (name, u kappa): (i) min(0.5, sqrt(||b||)) ||b|| (b = -grad E);
+    (ii) u kappa ||x_k||; (iii) u kappa ||b||."""
+    crit = getattr(st, "crit", None)
+    if crit is None:
+        return tol * st.bnorm
+    name, ukappa = crit
+    if name == "i":
+        return min(0.5, np.sqrt(st.bnorm)) * st.bnorm
+    if name == "ii":
+        return ukappa * float(np.linalg.norm(st.x))
+    return ukappa * st.bnorm
+
+
 class PCGState:
     """Saved PCG state so App. B's 'return to PCG for an additional 100 iterations' can resume."""
 
@@ -110,7 +125,7 @@ def pcg_run(A, Dinv, st: PCGState, tol, window, max_iters, literal_stall=False):
         if not np.isfinite(rn):
             st.stop = STOP_NAN
             return st
-        if rn <= tol * st.bnorm:
+        if rn <= stop_threshold(st, tol):
             st.stop = STOP_CONVERGED
             return st
         k = st.k
@@ -145,8 +160,9 @@ def stop_margin(st, tol):
     return min(abs(h / ref - 1.0) for h in st.hist[-2:])
 
 
-def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False):
+def pcg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False, crit=None):
     st = pcg_start(A, b, x0, Dinv)
+    st.crit = crit
     return pcg_run(A, Dinv, st, tol, window, max_iters, literal_stall)
 
 
@@ -182,7 +198,7 @@ def cg_run(A, Dinv, st, tol, window, max_iters, literal_stall=False):
         if not np.isfinite(rn):
             st.stop = STOP_NAN
             return st
-        if rn <= tol * st.bnorm:
+        if rn <= stop_threshold(st, tol):
             st.stop = STOP_CONVERGED
             return st
         if stalled(st, window, literal_stall):
@@ -210,8 +226,10 @@ def cg_run(A, Dinv, st, tol, window, max_iters, literal_stall=False):
         st.z = st.u
 
 
-def pcg_cg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False):
-    return cg_run(A, Dinv, cg_start(A, b, x0, Dinv), tol, window, max_iters, literal_stall)
+def pcg_cg(A, b, x0, Dinv, tol=1e-4, window=100, max_iters=20000, literal_stall=False, crit=None):
+    st = cg_start(A, b, x0, Dinv)
+    st.crit = crit
+    return cg_run(A, Dinv, st, tol, window, max_iters, literal_stall)
 
 
 def warm_start(A, b, groups, Dinv, fixed, tol=1e-2, max_iters=100):

@@ -13,7 +13,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (BAL_ADDITIVE_PRECOND, BAL_CCD_LITERAL, BAL_FP32_MATRIX, BAL_FRICTION_LAGGED, BAL_FRICTION_NO_FREEZE, BAL_PCG_LITERAL_STALL, BAL_NO_AUGLAG, BAL_NO_WARMSTART, BAL_SIGMA_CAP,
+from ._lib import (BAL_ADDITIVE_PRECOND, BAL_PCG_CRIT_I, BAL_PCG_CRIT_II, BAL_PCG_CRIT_III, BAL_CCD_LITERAL, BAL_FP32_MATRIX, BAL_FRICTION_LAGGED, BAL_FRICTION_NO_FREEZE, BAL_PCG_LITERAL_STALL, BAL_NO_AUGLAG, BAL_NO_WARMSTART, BAL_SIGMA_CAP,
                    BAL_SIGMA_MIN, STATUS, bal_bsr_host, bal_contact_state, bal_dist, bal_material, bal_mesh,
                    bal_params, bal_pcg_opts, bal_pcg_stats, bal_step_stats, bal_system_view)
 
@@ -21,7 +21,7 @@ __all__ = ["BalError", "BalCtx", "bal_init", "bal_step", "bal_step_host", "bal_a
            "bal_load_bsr", "bal_bench_spmv", "bal_destroy", "bal_nccl_unique_id", "bal_dist_info", "bal_spmv_rows",
            "bal_halo_plan", "bal_halo_pack", "bal_halo_unpack", "bal_get_system", "BAL_NO_WARMSTART", "BAL_NO_AUGLAG",
            "BAL_FRICTION_LAGGED", "BAL_SIGMA_CAP", "BAL_SIGMA_MIN", "BAL_FRICTION_NO_FREEZE", "BAL_CCD_LITERAL",
-           "BAL_PCG_LITERAL_STALL", "BAL_FP32_MATRIX", "BAL_ADDITIVE_PRECOND", "lib_path"]
+           "BAL_PCG_LITERAL_STALL", "BAL_FP32_MATRIX", "BAL_ADDITIVE_PRECOND", "BAL_PCG_CRIT_I", "BAL_PCG_CRIT_II", "BAL_PCG_CRIT_III", "lib_path"]
 
 lib_path = _lib.LIB_PATH
 

@@ -33,6 +33,9 @@ BAL_CCD_LITERAL = 64
 BAL_PCG_LITERAL_STALL = 128
 BAL_FP32_MATRIX = 256
 BAL_ADDITIVE_PRECOND = 512
+BAL_PCG_CRIT_I = 1024
+BAL_PCG_CRIT_II = 2048
+BAL_PCG_CRIT_III = 4096
 
 
 class bal_mesh(C.Structure):

@@ -452,7 +452,7 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->y.reserve(3 * (size_t)N);
   c->xt.reserve(3 * (size_t)N);
   for (auto* b : {&c->pr, &c->pz, &c->pp, &c->pq, &c->px, &c->ps, &c->tmp_a, &c->tmp_b}) b->reserve(3 * (size_t)N);
-  c->upart.reserve(2 * (size_t)kVecBlocks);
+  c->upart.reserve(3 * (size_t)kVecBlocks);  // (r,u), (r,r) pairs + (x,x) for App. B criterion (ii)
   c->dpart.reserve(4 * (size_t)kSMs);
   c->partials.reserve((size_t)kRedBlocks * kMaxGroups * 4 + 16 * kSMs * 4);
   c->red.reserve(kRedBlocks + 16);  // [0, kRedBlocks) partials, then scalar outputs

@@ -107,7 +107,8 @@ struct bal_ctx {
   int ngroups = 0;
   bal::DevBuf<double> as_inv;  // BAL_ADDITIVE_PRECOND: [n_agg][27][27] level-2 inverses (App. A)
   bool as_ready = false;       // as_inv holds the inverses of the current system
-  bool ws_rejected = false;  // R-WS1: the last solve discarded its warm start
+  bool ws_rejected = false;
+  double last_ukappa = 0.0;  // u kappa of the last solve under App. B criteria (ii)/(iii)  // R-WS1: the last solve discarded its warm start
   // scratch
   bal::DevBuf<double> tmp_a, tmp_b, red;
   bal::DevBuf<int> tmp_i;

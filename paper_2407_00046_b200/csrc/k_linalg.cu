@@ -650,8 +650,9 @@ void launch_pcg_pupdate(cudaStream_t st, int n, const double* z, double* p, cons
 __global__ void __launch_bounds__(kVecThreads)
 k_cg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, const double* __restrict__ dinv,
           double* __restrict__ r, double* __restrict__ u, double* __restrict__ p, double* __restrict__ s,
-          double* __restrict__ upart, double* partials, unsigned* counter, PcgScal* sc, double* hist) {
-  double g = 0.0, rr = 0.0, bb = 0.0;
+          double* __restrict__ upart, double* partials, unsigned* counter, PcgScal* sc, double* hist,
+          const double* __restrict__ x) {
+  double g = 0.0, rr = 0.0, bb = 0.0, xx = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     double rv[3];
 #pragma unroll
@@ -663,6 +664,7 @@ k_cg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, c
       p[j] = 0.0;
       s[j] = 0.0;
       bb += bj * bj;
+      if (x) xx += x[j] * x[j];
     }
     double u0, u1, u2;
     dinv_apply(dinv, i, rv[0], rv[1], rv[2], u0, u1, u2);
@@ -675,14 +677,17 @@ k_cg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, c
   __shared__ double sh[kVecThreads / 32];
   const double bg = block_sum<kVecThreads>(g, sh);
   const double br = block_sum<kVecThreads>(rr, sh);
+  const double bx = x ? block_sum<kVecThreads>(xx, sh) : 0.0;
   if (threadIdx.x == 0) {
     upart[2 * blockIdx.x] = bg;
     upart[2 * blockIdx.x + 1] = br;
+    if (x) upart[2 * kVecBlocks + blockIdx.x] = bx;
   }
   const double loc[1] = {bb};
   double tot[1];
   if (last_block_reduce<1, kVecThreads>(loc, partials, counter, tot) && threadIdx.x == 0) {
     sc->bnorm = sqrt(tot[0]);
+    if (sc->crit == 1) sc->tol = fmin(0.5, sqrt(sc->bnorm));  // App. B (i): min(0.5, sqrt||grad E||) ||grad E||
     sc->k = 0;
     sc->stop = -1;
     sc->done = 0;
@@ -693,8 +698,8 @@ k_cg_init(int n, const double* __restrict__ b, const double* __restrict__ Ax0, c
 
 void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
                     double* u, double* p, double* s, double* upart, double* partials, unsigned* counter,
-                    PcgScal* sc, double* hist) {
-  k_cg_init<<<kVecBlocks, kVecThreads, 0, st>>>(n, b, Ax0, dinv, r, u, p, s, upart, partials, counter, sc, hist);
+                    PcgScal* sc, double* hist, const double* x) {
+  k_cg_init<<<kVecBlocks, kVecThreads, 0, st>>>(n, b, Ax0, dinv, r, u, p, s, upart, partials, counter, sc, hist, x);
   CK(cudaGetLastError());
 }
 
@@ -704,7 +709,7 @@ template <int NP>
 BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* __restrict__ pin_ptr,
                            const double* __restrict__ part, const double* __restrict__ w, double* __restrict__ u,
                            double* __restrict__ p, double* __restrict__ s, double* __restrict__ x,
-                           double* __restrict__ r, double alpha, double beta, double& g, double& rr) {
+                           double* __restrict__ r, double alpha, double beta, double& g, double& rr, double& xx) {
   constexpr int ND = 3 * NP;
   const size_t d0 = 3 * (size_t)i0;
   double wv[ND], uv[ND], pv[ND], sv[ND], xv[ND], rv[ND];
@@ -747,6 +752,7 @@ BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* _
     sv[k] = wv[k] + beta * sv[k];
     xv[k] = xv[k] + alpha * pv[k];
     rv[k] = rv[k] - alpha * sv[k];
+    xx += xv[k] * xv[k];
   }
 #pragma unroll
   for (int n = 0; n < NP; ++n) {
@@ -777,7 +783,7 @@ k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_
             double* __restrict__ x, double* __restrict__ r, double* __restrict__ upart, PcgScal* sc) {
   if (sc->done) return;
   const double alpha = sc->alpha, beta = sc->beta;
-  double g = 0.0, rr = 0.0;
+  double g = 0.0, rr = 0.0, xx = 0.0;
   // 16-byte alignment of every vector (cudaMalloc / torch allocations); else one node per thread
   const bool vec = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(p) |
                      reinterpret_cast<uintptr_t>(s) | reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(r)) &
@@ -785,17 +791,20 @@ k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_
   const int T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
   if (vec) {
     const int npairs = n / 2;
-    for (int q = t; q < npairs; q += T) cg_update_nodes<2>(2 * q, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
-    if ((n & 1) && t == T - 1) cg_update_nodes<1>(n - 1, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
+    for (int q = t; q < npairs; q += T) cg_update_nodes<2>(2 * q, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
+    if ((n & 1) && t == T - 1) cg_update_nodes<1>(n - 1, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
   } else {
-    for (int i = t; i < n; i += T) cg_update_nodes<1>(i, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr);
+    for (int i = t; i < n; i += T) cg_update_nodes<1>(i, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
   }
   __shared__ double sh[kVecThreads / 32];
   const double bg = block_sum<kVecThreads>(g, sh);
   const double br = block_sum<kVecThreads>(rr, sh);
+  const bool wx = sc->crit == 2;
+  const double bx = wx ? block_sum<kVecThreads>(xx, sh) : 0.0;
   if (threadIdx.x == 0) {
     upart[2 * blockIdx.x] = bg;
     upart[2 * blockIdx.x + 1] = br;
+    if (wx) upart[2 * kVecBlocks + blockIdx.x] = bx;
     if (blockIdx.x == 0) sc->k = sc->k + 1;  // read by the next SpMV's last CTA only
   }
 }

@@ -575,17 +575,20 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
     __syncthreads();
     if (last) {
       __threadfence();
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      const bool wx = a.sc->crit == 2;  // criterion (ii) needs ||x_k||: (x,x) partials after the pairs
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
       for (int i = tid; i < G; i += kTsThreads) t0 += a.dpart[i];
       for (int i = tid; i < kVecBlocks; i += kTsThreads) {
         t1 += a.upart[2 * i];
         t2 += a.upart[2 * i + 1];
+        if (wx) t3 += a.upart[2 * kVecBlocks + i];
       }
       const double delta = block_sum<kTsThreads>(t0, sh);
       const double gam = block_sum<kTsThreads>(t1, sh);
       const double rr = block_sum<kTsThreads>(t2, sh);
+      const double xx = wx ? block_sum<kTsThreads>(t3, sh) : 0.0;
       if (tid == 0) {
-        cg_scalars(a.sc, a.hist, gam, rr, delta);
+        cg_scalars(a.sc, a.hist, gam, rr, delta, xx);
         *a.counter = 0u;
       }
     }

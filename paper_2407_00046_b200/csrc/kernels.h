@@ -136,7 +136,7 @@ void launch_as_apply(cudaStream_t st, int N, const double* inv, const double* r,
 // Chronopoulos-Gear PCG (k_linalg.cu): init from A x0 (complete) and the per-iteration update
 void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, const double* dinv, double* r,
                     double* u, double* p, double* s, double* upart, double* partials, unsigned* counter,
-                    PcgScal* sc, double* hist);
+                    PcgScal* sc, double* hist, const double* x);
 void launch_cg_update(cudaStream_t st, int n, const double* dinv, const int* pin_ptr, const double* part,
                       const double* w, double* u, double* p, double* s, double* x, double* r, double* upart,
                       PcgScal* sc);
@@ -162,6 +162,11 @@ struct PcgScal {
   int lit;      // BAL_PCG_LITERAL_STALL: Q15 residual-minimum stagnation test instead of R-PCG1
   double stall_rel;  // R-PCG1 threshold (kStallRel)
   double pmin;  // literal test: min ||r_j|| over j <= k - window (maintained incrementally)
+  // NEXT-4 App. B alternative criteria: 0 = ||r|| <= tol ||b|| (the paper's); 1 = (i) truncated
+  // Newton, tol = min(0.5, sqrt(||b||)); 2 = (ii) ||r|| <= u kappa ||x_k||; 3 = (iii) tol = u kappa
+  int crit;
+  double ukappa;  // u kappa(A), kappa from the assembled eigenvalues (DESIGN.md R-KAPPA)
+  double xx;      // ||x_k||^2 (criterion (ii); from the update kernels' (x,x) block partials)
 };
 constexpr double kStallRel = 1e-10;  // DESIGN.md R-PCG1
 // R-PCG1 threshold; BAL_STALL_REL overrides it (experiments)

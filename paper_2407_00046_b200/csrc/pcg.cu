@@ -1,11 +1,14 @@
 // pcg.cu -- host drivers of the warm start (Q20) and the global block-Jacobi PCG with
 // the App. B policy (Q14-Q16).  All scalars stay on the device; the host only polls
 // the device `done` flag once per batch of kBatch iterations (kernels early-exit once done).
+#include <cfloat>
 #include <climits>
+#include <vector>
 #include <cmath>
 #include <cstring>
 
 #include "ctx.h"
+#include "reduce.cuh"
 
 namespace bal {
 
@@ -77,6 +80,49 @@ static void as_build(bal_ctx* c) {
 }
 
 static bool as_on(const bal_ctx* c) { return (c->prm.flags & BAL_ADDITIVE_PRECOND) != 0; }
+
+// NEXT-4: App. B's alternative PCG criteria selected by flags (0 = the paper's relative residual)
+static int pcg_crit(const bal_ctx* c) {
+  const uint32_t f = c->prm.flags;
+  return (f & BAL_PCG_CRIT_I) ? 1 : (f & BAL_PCG_CRIT_II) ? 2 : (f & BAL_PCG_CRIT_III) ? 3 : 0;
+}
+
+__global__ void k_free_minmax(int n, const double* __restrict__ e, const int* __restrict__ group,
+                              double* __restrict__ part) {
+  __shared__ double sh[256 / 32];
+  double lo = INFINITY, hi = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (group[i] != INT_MIN) {
+      lo = fmin(lo, e[i]);
+      hi = fmax(hi, e[i]);
+    }
+  const double a = block_min<256>(lo, sh);
+  const double b = -block_min<256>(-hi, sh);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// kappa(A) estimated from the assembled eigenvalues ("approximating the condition number ...
+// using our assembled eigenvalues across elasticity, collision stencils and diagonal mass matrix";
+// DESIGN.md R-KAPPA): max_j e_j / min_j e_j over free nodes (Lambda is constant over a node's DOFs)
+static double kappa_estimate(bal_ctx* c) {
+  if (c->loaded_bsr) throw std::invalid_argument("App. B criteria (ii)/(iii) need an assembled system");
+  cudaStream_t st = c->st;
+  c->red.reserve(2 * kRedBlocks);
+  k_free_minmax<<<kRedBlocks, 256, 0, st>>>(c->N, c->e_node.ptr, c->group.ptr, c->red.ptr);
+  std::vector<double> h(2 * kRedBlocks);
+  CK(cudaMemcpyAsync(h.data(), c->red.ptr, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  c->launches += 1;
+  double lo = INFINITY, hi = 0.0;
+  for (int b = 0; b < kRedBlocks; ++b) {
+    lo = std::min(lo, h[2 * b]);
+    hi = std::max(hi, h[2 * b + 1]);
+  }
+  return (lo > 0.0 && std::isfinite(lo)) ? hi / lo : 1.0;
+}
 
 // One batch = kBatch PCG iterations (SpMV+dot, update, p-update) + a D2H copy of the scalars and a
 // completion event, captured once per solve into a CUDA graph.  Two graphs (ping-pong event sets
@@ -266,6 +312,14 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   h.lit = (c->prm.flags & BAL_PCG_LITERAL_STALL) ? 1 : 0;
   h.pmin = INFINITY;
   h.stall_rel = stall_rel();
+  h.crit = pcg_crit(c);
+  if (h.crit) {
+    if (!ts_usable(S))
+      throw std::invalid_argument("App. B criteria (i)-(iii) need the single-GPU tile-SpMV (Chronopoulos-Gear) path");
+    if (h.crit >= 2) h.ukappa = DBL_EPSILON * kappa_estimate(c);
+    if (h.crit == 3) h.tol = h.ukappa;
+    c->last_ukappa = h.ukappa;
+  }
   CK(cudaMemcpyAsync(c->scal.ptr, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   if (as_on(c)) {
     if (!ts_usable(S))
@@ -276,7 +330,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
   if (ts_usable(S)) {
     // single-reduction (Chronopoulos-Gear) PCG: init, then SpMV 0 (w_0 = A u_0, stop test at k = 0)
     launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
-                   c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+                   c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr, c->px.ptr);
     if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, nullptr);
     if (warm && ws_guard_rejects(c, rhs)) {
       // DESIGN.md R-WS1: the warm start is used only when it is closer to the solution than x = 0 in the
@@ -284,7 +338,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
       CK(cudaMemsetAsync(c->px.ptr, 0, 3 * (size_t)N * sizeof(double), st));
       CK(cudaMemsetAsync(c->pq.ptr, 0, 3 * (size_t)N * sizeof(double), st));
       launch_cg_init(st, N, rhs, c->pq.ptr, c->dinv.ptr, c->pr.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr, c->upart.ptr,
-                     c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr);
+                     c->partials.ptr, c->counter.ptr, c->scal.ptr, c->hist.ptr, c->px.ptr);
       if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, nullptr);
       c->launches += 1;
       c->ws_rejected = true;
@@ -318,6 +372,7 @@ int pcg_solve(bal_ctx* c, const double* rhs, const double* x0, double* x_out, bo
 // App. B: "return to the PCG method for an additional 100 iterations" from the saved state.
 __global__ void k_set_resume(PcgScal* sc, int extra, int cap) {
   sc->tol = 0.0;
+  sc->crit = 0;  // App. B resume: exactly `extra` more iterations whatever the criterion
   sc->window = 0;
   sc->max_iters = min(sc->k + extra, cap);
   sc->done = (sc->k >= sc->max_iters) ? 1 : 0;

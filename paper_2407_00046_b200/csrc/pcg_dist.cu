@@ -417,8 +417,8 @@ void dist_init(bal_ctx* c, const bal_dist* dd) {
     throw std::invalid_argument("bal_init: world > 1 needs nccl_unique_id or a host transport");
   d.active = d.world > 1 || host_tp || dd->nccl_unique_id != nullptr;
   if (!d.active) return;
-  if (c->prm.flags & BAL_ADDITIVE_PRECOND)
-    throw std::invalid_argument("bal_init: BAL_ADDITIVE_PRECOND is single-GPU only");
+  if (c->prm.flags & (BAL_ADDITIVE_PRECOND | BAL_PCG_CRIT_I | BAL_PCG_CRIT_II | BAL_PCG_CRIT_III))
+    throw std::invalid_argument("bal_init: BAL_ADDITIVE_PRECOND / BAL_PCG_CRIT_* are single-GPU only");
   if (!host_tp) {
     ncclUniqueId id;
     std::memcpy(&id, dd->nccl_unique_id, sizeof(id));

@@ -54,7 +54,8 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
     sc->done = 1;
     return;
   }
-  if (rn <= sc->tol * sc->bnorm) {
+  const double thr = sc->crit == 2 ? sc->ukappa * sqrt(sc->xx) : sc->tol * sc->bnorm;
+  if (rn <= thr) {
     sc->stop = 0;
     sc->done = 1;
     return;
@@ -91,8 +92,9 @@ BAL_D void pcg_stop_check(PcgScal* sc, const double* hist) {
 // beta_k = gam_k / gam_{k-1}, alpha_k = gam_k / (delta_k - beta_k gam_k / alpha_{k-1}) -- computed
 // even when the solve stops, so an App. B resume continues with the update of step k.  The CG
 // objective decreases by alpha_{k-1} gam_{k-1} / 2 in step k-1 (R-PCG1 bookkeeping).
-BAL_D void cg_scalars(PcgScal* sc, double* hist, double gam, double rr, double delta) {
+BAL_D void cg_scalars(PcgScal* sc, double* hist, double gam, double rr, double delta, double xx = 0.0) {
   const int k = sc->k;
+  sc->xx = xx;
   if (k > 0) sc->dec += 0.5 * sc->alpha * sc->rz;
   sc->rr = rr;
   hist[k] = sqrt(rr);

@@ -266,3 +266,31 @@ def test_additive_schwarz_is_the_printed_sum_and_its_special_cases():
         a = la.pcg_cg(A, b, np.zeros(n), M, tol=0.0, window=10 ** 9, max_iters=k)
         t = la.pcg(A, b, np.zeros(n), M, tol=0.0, window=10 ** 9, max_iters=k)
         assert np.linalg.norm(a.x - t.x) <= 1e-10 * np.linalg.norm(t.x)
+
+
+def test_app_b_alternative_criteria_stop_where_defined():
+    """NEXT-4, App. B (P:753) criteria (i) ||r|| <= min(0.5, sqrt||b||) ||b||, (ii) ||r_k|| <=
+    u kappa ||x_k||, (iii) ||r_k|| <= u kappa ||b|| in both PCG forms: each stops at the FIRST
+    iteration whose residual meets its threshold (checked from outside: the run capped one iteration
+    earlier does not meet it), and (iii) with u kappa = tol is the default relative-residual test."""
+    rng = np.random.default_rng(41)
+    bs = _rand_spd_blocks(rng, 30, cond_scale=1e4)
+    A = bs.to_csr()
+    Dinv = np.linalg.inv(bs.diag_blocks())
+    n = A.shape[0]
+    for scale in (1e-3, 1e2):  # sqrt||b|| below and above 0.5 for criterion (i)
+        b = scale * rng.normal(size=n)
+        bn = np.linalg.norm(b)
+        for solve in (la.pcg, la.pcg_cg):
+            for crit, thr in ((("i", 0.0), lambda st: min(0.5, np.sqrt(bn)) * bn),
+                              (("ii", 1e-9), lambda st: 1e-9 * np.linalg.norm(st.x)),
+                              (("iii", 1e-7), lambda st: 1e-7 * bn)):
+                st = solve(A, b, np.zeros(n), Dinv, tol=1e-4, window=10 ** 9, crit=crit)
+                assert st.stop == la.STOP_CONVERGED
+                assert st.hist[-1] <= thr(st)
+                if st.k > 0:
+                    prev = solve(A, b, np.zeros(n), Dinv, tol=1e-4, window=10 ** 9, max_iters=st.k - 1, crit=crit)
+                    assert prev.stop == la.STOP_CAP and prev.hist[-1] > thr(prev)
+        a = la.pcg(A, b, np.zeros(n), Dinv, tol=1e-4, window=10 ** 9, crit=("iii", 1e-4))
+        d = la.pcg(A, b, np.zeros(n), Dinv, tol=1e-4, window=10 ** 9)
+        assert a.k == d.k and np.array_equal(a.x, d.x)

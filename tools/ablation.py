@@ -22,7 +22,11 @@ VARIANTS = {"bal+warmstart": 0, "bal, no warm start": bal.BAL_NO_WARMSTART,
             "sigma min(1.2 sigma, 100 sigma0)": bal.BAL_SIGMA_MIN,
             "additive precond (App. A) alone": bal.BAL_ADDITIVE_PRECOND | bal.BAL_NO_WARMSTART,
             "additive precond + warm start": bal.BAL_ADDITIVE_PRECOND,
-            "fp32 matrix storage (NEXT-3)": bal.BAL_FP32_MATRIX}
+            "fp32 matrix storage (NEXT-3)": bal.BAL_FP32_MATRIX,
+            "App. B criterion (i) truncated Newton": bal.BAL_PCG_CRIT_I,
+            "App. B criterion (ii) u kappa ||x||": bal.BAL_PCG_CRIT_II,
+            "App. B criterion (iii) u kappa ||b||": bal.BAL_PCG_CRIT_III}
+ONLY = os.environ.get("BAL_ABL_ONLY")  # comma-separated substrings: run only the matching variants
 
 
 def run(sc, flags, frames=None, newton=None):
@@ -59,6 +63,8 @@ def main():
     sc = {"c1": lambda: scenes.make_cubes(1), "c2": lambda: scenes.make_armadillo_like(2),
           "c3": lambda: scenes.make_impact(3), "c4": lambda: scenes.make_puffer_net(seed=4)}[which]()
     for name, fl in VARIANTS.items():
+        if ONLY and not any(k in name for k in ONLY.split(",")):
+            continue
         try:
             r = run(sc, fl, newton=k) if which == "c4" else run(sc, fl, frames=k)
         except bal.BalError as e:  # a variant that fails (e.g. NaN) is reported, not fatal
