@@ -58,11 +58,16 @@ def test_criterion_stop_matches_the_oracle(state, name, gflag, oflag):
     assert s["stop_reason"] == st.stop
     assert abs(s["iters"] - st.k) <= max(1, 0.02 * st.k), (s["iters"], st.k)
     x = xg.cpu().numpy()
-    rn = np.linalg.norm(b - asm["A"] @ x)
-    thr = {"i": min(0.5, np.sqrt(np.linalg.norm(b))) * np.linalg.norm(b), "ii": ukappa * np.linalg.norm(x),
-           "iii": ukappa * np.linalg.norm(b)}[name]
-    if st.stop == la.STOP_CONVERGED:
-        assert rn <= 1.01 * thr  # true residual vs the recursive one the test used
+    if name == "i":
+        # (i) stops early (a loose threshold): the true residual meets it too
+        rn = np.linalg.norm(b - asm["A"] @ x)
+        assert rn <= 1.01 * min(0.5, np.sqrt(np.linalg.norm(b))) * np.linalg.norm(b)
+        assert np.linalg.norm(x - st.x) <= 1e-8 * np.linalg.norm(st.x)
+    else:
+        # (ii) / (iii): u kappa thresholds lie below the attainable accuracy of the true residual
+        # (~u |A| |x|); only the recursive residual meets them (on both sides), and both solutions
+        # have converged to rounding: compare them
+        assert np.linalg.norm(x - st.x) <= 1e-6 * np.linalg.norm(st.x)
 
 
 @pytest.mark.parametrize("name,gflag,oflag", CRITS)
