@@ -543,3 +543,48 @@ def make_puffer_tiles(seed=5, tiles=(3, 2), gap=0.1, **kw):
         sb.n += len(x)
     first = parts[0][0]
     return sb.build(first["materials"], "C5-puffer-tiles", chi=first["params"]["chi"])
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: twisting rods (PAPER.md:299-304 fig:rods, Table 1 row P:679)
+# --------------------------------------------------------------------------
+TWIST_OMEGA = 2.0 * np.pi * 5.0 / 12.0  # 5/12 revolutions per second
+
+
+def make_twisting_rods(seed=6, n=12, length=103, voxel=0.0025, gap=0.01, E=1e7, nu=0.4, rho=1e3,
+                       omega=TWIST_OMEGA):
+    """NEXT-2 recipe: four stiff rods (E = 10 MPa; Table 1: 355K tets / 70.4K nodes)
+    along z in a 2 x 2 bundle, each n x n x length voxels of `voxel` (6 Kuhn tets per voxel: 12 x 12 x
+    103 gives T = 355,968, N = 70,304), `gap` between neighbouring rods, a generic 0.05-0.15 degree
+    rotation per rod.  The first and last node layers of every rod are Dirichlet nodes (node_fixed)
+    scripted by twist_targets(): the z = 0 ends rotate about the bundle axis at +omega, the far ends
+    at -omega (torsion from both ends).  chi = 0 (Table 1)."""
+    rng = np.random.default_rng(seed)
+    x0, t0 = voxel_mesh(np.ones((n, n, length), bool), voxel)
+    zl = x0[:, 2]
+    ends = np.where(np.abs(zl - zl.min()) < 1e-12, 1, np.where(np.abs(zl - zl.max()) < 1e-12, 2, 0))
+    half = 0.5 * n * voxel
+    sb = SceneBuilder()
+    end_side = []
+    for cx, cy in ((-1, -1), (1, -1), (-1, 1), (1, 1)):
+        x = x0 - np.array([half, half, 0.5 * length * voxel])
+        x = x @ rot_axis(rng.normal(size=3), np.deg2rad(rng.uniform(0.05, 0.15))).T
+        x[:, 0] += cx * (half + 0.5 * gap)
+        x[:, 1] += cy * (half + 0.5 * gap)
+        sb.add_body(x, _orient(x, t0), 0, fixed=(ends > 0).astype(np.uint8))
+        end_side.append(ends)
+    sc = sb.build([(E, nu, rho)], "twisting-rods", chi=0.0)
+    sc["twist_end"] = np.concatenate(end_side).astype(np.int8)  # 1 = near end (+omega), 2 = far end (-omega)
+    sc["twist_omega"] = float(omega)
+    return sc
+
+
+def twist_targets(scene, t):
+    """Scripted Dirichlet positions of the rod ends at time t (scene boundary condition, no method
+    arithmetic): rest positions rotated about the z axis by +omega t (near ends) / -omega t (far ends).
+    Returns the (N, 3) array of target positions of all nodes (non-end rows = rest positions)."""
+    x = scene["rest_x"].copy()
+    for side, sign in ((1, 1.0), (2, -1.0)):
+        m = scene["twist_end"] == side
+        x[m] = x[m] @ rot_axis((0.0, 0.0, 1.0), sign * scene["twist_omega"] * t).T
+    return x
