@@ -20,7 +20,7 @@ LIMIT = float(sys.argv[2]) if len(sys.argv) > 2 else 900.0
 OUT = sys.argv[3] if len(sys.argv) > 3 else None
 sc = scenes.make_twisting_rods()
 dev = torch.device("cuda:0")
-ctx = bal.bal_init(sc)
+ctx = bal.bal_init(sc, flags=int(os.environ.get("BAL_FLAGS", "0")))
 h = sc["params"]["h"]
 fixed = sc["node_fixed"].astype(bool)
 x = sc["x0"].copy()
@@ -49,7 +49,7 @@ for k in range(F):
     if time.time() - t_start > LIMIT:
         break
 ok = [f for f in frames if "error" not in f]
-summ = {"scene": "twisting-rods", "tets": len(sc["tets"]), "nodes": len(sc["x0"]), "frames": len(ok),
+summ = {"scene": "twisting-rods", "flags": int(os.environ.get("BAL_FLAGS", "0")), "tets": len(sc["tets"]), "nodes": len(sc["x0"]), "frames": len(ok),
         "seconds_per_frame": float(np.mean([f["seconds"] for f in ok[1:]])) if len(ok) > 1 else None,
         "newton_per_frame": float(np.mean([f["newton_iters"] for f in ok])) if ok else None,
         "max_constraints": max([f["max_constraints"] for f in ok], default=0),
