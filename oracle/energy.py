@@ -5,6 +5,10 @@ TEST INFRASTRUCTURE (see oracle/__init__.py).
 Inertia   E_I = sum_j m_j ||x_j - y_j||^2 / (2 h^2)           PAPER.md:143 (§3.1)
 Elastic   Psi = sum_e V_e [mu/2 (tr F^T F - 3) - mu ln J + lam/2 (ln J)^2],  F = D_s D_m^{-1}
           (+inf if J <= 0)                                      SURVEY Q1 reading of "Neo-Hookean"
+          ARAP tets (NEXT-4; DESIGN.md R-ARAP): Psi = mu ||F - R||_F^2, R the rotation of
+          the polar decomposition F = R S, = mu (tr F^T F - 2 tr S + 3); tr S = sigma_1 + sigma_2 +
+          sigma_3 is the largest root of s^4 - 2 I1 s^2 - 8 J s + I1^2 - 4 I2 = 0 (I1 = tr C, I2 = the
+          second invariant of C = F^T F, J = det F), reached by Newton in AD arithmetic (+inf if J <= 0)
 Barrier   b(d, dhat) = -(d - dhat)^2 ln(d / dhat) for 0 < d < dhat, else 0
                                                                 PAPER.md:193-200 (eq:IPC-barrier)
 Mollifier f(y) = -y^3/(3 eps^2) + y^2/eps (y < eps), y - eps/3 (y >= eps), eps = eps_v h
@@ -54,19 +58,55 @@ def _nh_psi_ad(xs, Dm_inv, vol, mu, lam):
     return psi * vol
 
 
+def _arap_psi_ad(xs, Dm_inv, vol, mu, newton=4):
+    """xs: 12 D2 variables; returns D2 of V * mu ||F - R||^2 = V mu (I1 - 2 tr S + 3)."""
+    p = [xs[3 * k:3 * k + 3] for k in range(4)]
+    Ds = [[p[c + 1][r] - p[0][r] for c in range(3)] for r in range(3)]
+    F = [[Ds[r][0] * Dm_inv[:, 0, c] + Ds[r][1] * Dm_inv[:, 1, c] + Ds[r][2] * Dm_inv[:, 2, c]
+          for c in range(3)] for r in range(3)]
+    J = (F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1])
+         - F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0])
+         + F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]))
+    # C = F^T F, I1 = tr C, I2 = (I1^2 - tr C^2) / 2
+    Cm = [[F[0][i] * F[0][j] + F[1][i] * F[1][j] + F[2][i] * F[2][j] for j in range(3)] for i in range(3)]
+    I1 = Cm[0][0] + Cm[1][1] + Cm[2][2]
+    trC2 = None
+    for i in range(3):
+        for j in range(3):
+            t = Cm[i][j] * Cm[j][i]
+            trC2 = t if trC2 is None else trC2 + t
+    I2 = (I1 * I1 - trC2) * 0.5
+    # tr S: start from the sum of singular values of the values, then Newton on the quartic in AD
+    Fv = np.stack([np.stack([F[r][c].v for c in range(3)], -1) for r in range(3)], -2)
+    s = J.const_like(np.linalg.svd(Fv, compute_uv=False).sum(axis=-1))
+    for _ in range(newton):
+        s2 = s * s
+        f = s2 * s2 - I1 * s2 * 2.0 - J * s * 8.0 + I1 * I1 - I2 * 4.0
+        fp = s2 * s * 4.0 - I1 * s * 4.0 - J * 8.0
+        s = s - f / fp
+    psi = (I1 - s * 2.0 + 3.0) * mu + J.log() * 0.0  # + 0 * ln J: nan (infeasible) when J <= 0
+    return psi * vol
+
+
 def nh_stencils(x, mesh, chunk=20000):
-    """Per-tet AD value, gradient (T,12) and Hessian (T,12,12) of V_e Psi_e (no projection).
-    Tets with J <= 0 give nan (the caller treats the energy as +inf)."""
+    """Per-tet AD value, gradient (T,12) and Hessian (T,12,12) of V_e Psi_e (no projection): Neo-Hookean,
+    or ARAP for the tets mesh.arap marks.  Tets with J <= 0 give nan (the caller treats the energy as +inf)."""
     T = len(mesh.tets)
     val = np.empty(T)
     grad = np.empty((T, 12))
     hess = np.empty((T, 12, 12))
-    for s in range(0, T, chunk):
-        e = slice(s, min(T, s + chunk))
-        xs = x[mesh.tets[e]].reshape(-1, 12)
-        with np.errstate(invalid="ignore", divide="ignore"):
-            r = _nh_psi_ad(D2.variables(xs), mesh.Dm_inv[e], mesh.vol[e], mesh.mu[e], mesh.lam[e])
-        val[e], grad[e], hess[e] = r.v, r.g, r.H
+    arap = mesh.arap if mesh.arap is not None else np.zeros(T, bool)
+    for model in (False, True):
+        idx = np.nonzero(arap == model)[0]
+        for s in range(0, len(idx), chunk):
+            e = idx[s:s + chunk]
+            xs = x[mesh.tets[e]].reshape(-1, 12)
+            with np.errstate(invalid="ignore", divide="ignore"):
+                if model:
+                    r = _arap_psi_ad(D2.variables(xs), mesh.Dm_inv[e], mesh.vol[e], mesh.mu[e])
+                else:
+                    r = _nh_psi_ad(D2.variables(xs), mesh.Dm_inv[e], mesh.vol[e], mesh.mu[e], mesh.lam[e])
+            val[e], grad[e], hess[e] = r.v, r.g, r.H
     return val, grad, hess
 
 
@@ -81,6 +121,10 @@ def nh_energy(x, mesh):
     Ic = np.einsum("eij,eij->e", F, F)
     lnJ = np.log(J)
     psi = mesh.mu / 2 * (Ic - 3.0) - mesh.mu * lnJ + mesh.lam / 2 * lnJ ** 2
+    if mesh.arap is not None and np.any(mesh.arap):
+        a = mesh.arap
+        trS = np.linalg.svd(F[a], compute_uv=False).sum(axis=-1)  # J > 0: tr S = sum of singular values
+        psi[a] = mesh.mu[a] * (Ic[a] - 2.0 * trS + 3.0)
     return float(np.sum(mesh.vol * psi))
 
 

@@ -32,6 +32,7 @@ class Mesh:
     tris: np.ndarray          # (F,3) surface triangles (outward) incl. obstacles
     edges: np.ndarray         # (E,2) unique surface edges (i<j)
     surf_verts: np.ndarray    # (V,) vertices of surface triangles
+    arap: np.ndarray = None   # (T,) bool: ARAP tet (NEXT-4, scene["material_model"] == 1), else Neo-Hookean
 
     @property
     def n(self):
@@ -89,4 +90,6 @@ def precompute(scene) -> Mesh:
     e = np.concatenate([tris[:, [0, 1]], tris[:, [1, 2]], tris[:, [2, 0]]], axis=0)
     e = np.unique(np.sort(e, axis=1), axis=0)
     sv = np.unique(tris.ravel())
-    return Mesh(X, tets, fixed, Dm_inv, vol, mu, lam, mass, tris, e, sv)
+    model = np.asarray(scene.get("material_model", np.zeros(len(mats))), np.int64).reshape(-1)
+    arap = model[tm] == 1 if len(tets) else np.zeros(0, bool)
+    return Mesh(X, tets, fixed, Dm_inv, vol, mu, lam, mass, tris, e, sv, arap)

@@ -180,3 +180,95 @@ def test_mollifier():
     q = w3[0] * w3[0] + w3[1] * w3[1] + w3[2] * w3[2]
     f0 = mollifier_of_sq_ad(q, eps)
     np.testing.assert_allclose(f0.H[0], 2 / eps * np.eye(3), rtol=1e-15)
+
+
+# ---------------------------------------------------------------- ARAP (NEXT-4, R-ARAP)
+def arap_tet_scene(X, E=1e5, nu=0.4, rho=1e3):
+    sc = one_tet_scene(X, E, nu, rho)
+    sc["material_model"] = np.array([1])
+    return sc
+
+
+def test_arap_is_zero_on_rotations_and_matches_scaling_closed_form():
+    """Psi = mu ||F - R||^2 vanishes with its gradient for EVERY rotation of the rest shape (not only
+    at rest); F = sI gives V * 3 mu (s - 1)^2 and gradient V P Dm^-T with P = 2 mu (s - 1) I."""
+    rng = np.random.default_rng(50)
+    for _ in range(5):
+        X = rand_tet(rng)
+        m = precompute(arap_tet_scene(X))
+        Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        Q *= np.sign(np.linalg.det(Q))
+        x = X @ Q.T + rng.normal(size=3)
+        v, g, _ = nh_stencils(x, m)
+        L = np.cbrt(m.vol[0])
+        assert abs(v[0]) < 1e-12 * m.mu[0] * m.vol[0] and np.max(np.abs(g)) <= 1e-12 * m.mu[0] * m.vol[0] / L
+        s = 1.0 + rng.uniform(-0.3, 0.5)
+        v, g, _ = nh_stencils(s * X, m)
+        assert v[0] == pytest.approx(m.vol[0] * 3 * m.mu[0] * (s - 1) ** 2, rel=1e-12)
+        Gd = m.vol[0] * 2 * m.mu[0] * (s - 1) * m.Dm_inv[0].T  # columns: nodes 1..3
+        np.testing.assert_allclose(g[0, 3:].reshape(3, 3), Gd.T, rtol=1e-11, atol=1e-12 * np.abs(Gd).max())
+
+
+def test_arap_rest_hessian_and_twist_eigenvalues():
+    """Rest Hessian = the linear-elastic tet stiffness with lam = 0 (||F - R||^2 -> eps:eps); at
+    F = diag(s1, s2, s3) (a tet with D_m = I) the F-space Hessian along the twist direction
+    e_i e_j^T - e_j e_i^T is V 4 mu (1 - 2 / (s_i + s_j)) (analytic ARAP eigensystem), and along the
+    scaling direction e_i e_i^T it is V 2 mu."""
+    rng = np.random.default_rng(51)
+    X = rand_tet(rng)
+    m = precompute(arap_tet_scene(X))
+    _, _, H = nh_stencils(X, m)
+    G = np.zeros((4, 3))
+    G[1:] = m.Dm_inv[0]
+    G[0] = -G[1:].sum(0)
+    K = np.zeros((12, 12))
+    for a in range(4):
+        for b in range(4):
+            K[3 * a:3 * a + 3, 3 * b:3 * b + 3] = m.vol[0] * m.mu[0] * (G[a] @ G[b] * np.eye(3) + np.outer(G[b], G[a]))
+    assert np.linalg.norm(H[0] - K) <= 1e-11 * np.linalg.norm(K)
+    X1 = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    m1 = precompute(arap_tet_scene(X1))
+    sig = np.array([0.7, 1.1, 1.6])
+    x = X1 * sig[None, :]  # F = diag(sig)
+    _, _, H = nh_stencils(x, m1)
+    HF = H[0][3:, 3:]  # F_rc = x[c+1][r]: index 3 c + r after dropping node 0
+    V, mu = m1.vol[0], m1.mu[0]
+    for i in range(3):
+        for j in range(i + 1, 3):
+            T = np.zeros((3, 3))
+            T[i, j], T[j, i] = 1.0, -1.0
+            t = T.T.ravel()  # t[3 c + r] = T[r, c]
+            assert t @ HF @ t == pytest.approx(V * 4 * mu * (1 - 2 / (sig[i] + sig[j])), rel=1e-10)
+        t = np.zeros(9)
+        t[3 * i + i] = 1.0
+        assert t @ HF @ t == pytest.approx(V * 2 * mu, rel=1e-10)
+
+
+def test_arap_fd_and_energy_consistency():
+    """AD gradient / Hessian vs central differences of the plain energy (nh_energy with the SVD) at
+    random deformations; J <= 0 is +inf like NH."""
+    rng = np.random.default_rng(52)
+    for _ in range(3):
+        X = rand_tet(rng)
+        m = precompute(arap_tet_scene(X))
+        x = X + 0.15 * rng.normal(size=X.shape)
+        v, g, H = nh_stencils(x, m)
+        assert v[0] == pytest.approx(nh_energy(x, m), rel=1e-12)
+        h = 1e-6
+        gfd = np.zeros(12)
+        for k in range(12):
+            xp, xm = x.copy().ravel(), x.copy().ravel()
+            xp[k] += h
+            xm[k] -= h
+            gfd[k] = (nh_energy(xp.reshape(4, 3), m) - nh_energy(xm.reshape(4, 3), m)) / (2 * h)
+        assert np.linalg.norm(gfd - g[0]) <= 1e-6 * np.linalg.norm(g[0])
+        Hfd = np.zeros((12, 12))
+        for k in range(12):
+            xp, xm = x.copy().ravel(), x.copy().ravel()
+            xp[k] += h
+            xm[k] -= h
+            Hfd[:, k] = (nh_stencils(xp.reshape(4, 3), m)[1][0] - nh_stencils(xm.reshape(4, 3), m)[1][0]) / (2 * h)
+        assert np.linalg.norm(Hfd - H[0]) <= 1e-6 * np.linalg.norm(H[0])
+    xi = X.copy()
+    xi[[1, 2]] = xi[[2, 1]]
+    assert nh_energy(xi, m) == np.inf
