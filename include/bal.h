@@ -56,7 +56,11 @@ typedef struct {
 } bal_mesh;
 
 /* Neo-Hookean material (Q1: Psi = mu/2 (tr F^T F - 3) - mu ln J + lam/2 (ln J)^2). */
-typedef struct { double E, nu, rho; } bal_material;
+/* Material (Table 1 columns E, nu, rho).  model: BAL_MODEL_NEO_HOOKEAN (Q1) or BAL_MODEL_ARAP
+ * (NEXT-4: Psi = mu ||F - R||_F^2, R the polar rotation; lambda unused; DESIGN.md R-ARAP). */
+#define BAL_MODEL_NEO_HOOKEAN 0
+#define BAL_MODEL_ARAP 1
+typedef struct { double E, nu, rho; int32_t model; } bal_material;
 
 /* Flags */
 #define BAL_NO_WARMSTART 1u  /* ablation: global PCG from x0 = 0 */

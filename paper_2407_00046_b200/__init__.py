@@ -129,7 +129,8 @@ def bal_init(scene, device=0, flags=0, params=None, rank=0, world=1, nccl_id=Non
     m.tet_material = _lib.ptr(mat, C.c_int32)
     m.n_obstacle_tris = len(ob) // 3
     m.obstacle_tris = _lib.ptr(ob, C.c_int32)
-    ma = (bal_material * len(mats))(*[bal_material(*row) for row in mats])
+    models = np.asarray(scene.get("material_model", np.zeros(len(mats))), np.int32).reshape(-1)
+    ma = (bal_material * len(mats))(*[bal_material(*row, int(mdl)) for row, mdl in zip(mats, models)])
     prm = make_params(params or scene["params"], flags)
     d = bal_dist()
     d.rank, d.world, d.device = int(rank), int(world), int(device)

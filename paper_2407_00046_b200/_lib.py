@@ -45,7 +45,7 @@ class bal_mesh(C.Structure):
 
 
 class bal_material(C.Structure):
-    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double)]
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double), ("model", C.c_int32)]
 
 
 class bal_params(C.Structure):

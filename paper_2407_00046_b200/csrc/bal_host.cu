@@ -168,6 +168,7 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->T = T;
   const double* X = m->rest_x;
   std::vector<double> Dm_inv(9 * (size_t)T), vol(T), mu(T), lam(T), mass(N, 0.0);
+  std::vector<unsigned char> tmodel(T, 0);
   std::vector<int4> tets(T);
   for (int e = 0; e < T; ++e) {
     int t[4];
@@ -200,6 +201,9 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
     const double E = mats[mi].E, nu = mats[mi].nu, rho = mats[mi].rho;
     mu[e] = E / (2.0 * (1.0 + nu));
     lam[e] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    if (mats[mi].model != BAL_MODEL_NEO_HOOKEAN && mats[mi].model != BAL_MODEL_ARAP)
+      throw std::invalid_argument("bal_init: unknown material model");
+    tmodel[e] = (unsigned char)mats[mi].model;
     for (int a = 0; a < 4; ++a) mass[t[a]] += rho * vol[e] / 4.0;
   }
   c->h_fixed.assign(m->node_fixed, m->node_fixed + N);
@@ -361,6 +365,8 @@ void precompute(bal_ctx* c, const bal_mesh* m, const bal_material* mats, int nma
   c->Dm_inv.upload(Dm_inv.data(), Dm_inv.size(), st);
   c->vol.upload(vol.data(), T, st);
   c->mu.upload(mu.data(), T, st);
+  c->any_arap = std::find(tmodel.begin(), tmodel.end(), (unsigned char)BAL_MODEL_ARAP) != tmodel.end();
+  if (c->any_arap) c->tmodel.upload(tmodel.data(), T, st);
   c->lam.upload(lam.data(), T, st);
   c->mass.upload(mass.data(), N, st);
   c->fixed.upload(c->h_fixed.data(), N, st);
@@ -474,7 +480,8 @@ namespace bal {
 void run_assembly(bal_ctx* c, const double* x, const double* y, double sigma) {
   cudaStream_t st = c->st;
   const int T = c->T, N = c->N;
-  launch_elastic(st, T, x, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr, c->stage_e.ptr,
+  launch_elastic(st, T, x, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr, c->any_arap ? c->tmodel.ptr : nullptr,
+                 c->stage_e.ptr,
                  c->grad_e.ptr, c->lbar_e.ptr);
   const int nc = c->cset.n, nf = c->n_fric, ns = nc + nf;
   c->n_contact = nc;

@@ -242,7 +242,8 @@ Energy energy(bal_ctx* c, StepWork& w, const double* xe, const Candidates& cand,
   // [7] sum |AL_i|
   CK(cudaMemsetAsync(E, 0, 8 * sizeof(double), st));
   if (T > 0) {
-    launch_elastic_energy(st, T, xe, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr, w.evals.ptr);
+    launch_elastic_energy(st, T, xe, c->tets.ptr, c->Dm_inv.ptr, c->vol.ptr, c->mu.ptr, c->lam.ptr,
+                          c->any_arap ? c->tmodel.ptr : nullptr, w.evals.ptr);
     launch_sum(st, T, w.evals.ptr, w.cw.part.ptr, E + 0);
   }
   k_inertia_energy<<<ceil_div(N, 256), 256, 0, st>>>(N, xe, c->y.ptr, c->mass.ptr, 0.5 / (h * h), c->fixed.ptr,

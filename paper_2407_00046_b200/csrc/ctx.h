@@ -73,6 +73,8 @@ struct bal_ctx {
   bal::DevBuf<float> lval32;  // BAL_FP32_MATRIX: FP32 copy of the stored blocks for k_spmv_ts
   bool sp_sym = false;
   TsDev sp_ts;
+  bal::DevBuf<unsigned char> tmodel;  // per tet: 0 Neo-Hookean, 1 ARAP (bal_material.model)
+  bool any_arap = false;
   // ---- elastic stencils
   bal::DevBuf<double> stage_e, grad_e, lbar_e;
   // ---- contact + friction stencils (friction appended after contact)

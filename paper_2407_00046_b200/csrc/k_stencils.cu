@@ -57,11 +57,85 @@ BAL_D void expand_write(const double (&PM)[Sym<3 * (K - 1)>::kSize], double* out
     for (int t = 0; t < 9; ++t) out[9 * ab + t] = 0.0;
 }
 
+// Eigen-decomposition of a symmetric 3x3 matrix a (full, in/out: diagonalised) by cyclic Jacobi in
+// registers; v: eigenvectors (columns).  Used for C = F^T F of ARAP tets (sigma_k^2 and V of the SVD).
+BAL_D void sym3_eig(double (&a)[3][3], double (&v)[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) v[i][j] = (i == j) ? 1.0 : 0.0;
+  const double fro2 = a[0][0] * a[0][0] + a[1][1] * a[1][1] + a[2][2] * a[2][2] +
+                      2.0 * (a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2]);
+  for (int sweep = 0; sweep < 20; ++sweep) {
+    const double off2 = 2.0 * (a[0][1] * a[0][1] + a[0][2] * a[0][2] + a[1][2] * a[1][2]);
+    if (!(off2 > 1e-32 * fro2)) break;
+#pragma unroll
+    for (int pq = 0; pq < 3; ++pq) {
+      const int p = pq == 2 ? 1 : 0, q = pq == 0 ? 1 : 2;
+      const double apq = a[p][q];
+      if (apq == 0.0) continue;
+      const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+      double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+      if (theta < 0.0) t = -t;
+      const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {  // A <- A J (columns p, q)
+        const double akp = a[k][p], akq = a[k][q];
+        a[k][p] = c * akp - sn * akq;
+        a[k][q] = sn * akp + c * akq;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {  // A <- J^T A (rows p, q)
+        const double apk = a[p][k], aqk = a[q][k];
+        a[p][k] = c * apk - sn * aqk;
+        a[q][k] = sn * apk + c * aqk;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double vkp = v[k][p], vkq = v[k][q];
+        v[k][p] = c * vkp - sn * vkq;
+        v[k][q] = sn * vkp + c * vkq;
+      }
+    }
+  }
+}
+
+// ARAP (NEXT-4, DESIGN.md R-ARAP): Psi = mu ||F - R||^2.  With C = F^T F = V diag(s^2) V^T (det V = 1)
+// and U = F V diag(1/s): R = U V^T, dPsi/dF = 2 mu (F - R), and the F-space Hessian
+// 2 mu (I - sum_{a<b} t_ab t_ab^T / (s_a + s_b)), t_ab = vec(u_a v_b^T - u_b v_a^T) (the twist modes).
+struct ArapSvd {
+  double s[3], U[3][3], V[3][3];
+};
+BAL_D ArapSvd arap_svd(const double (&F)[3][3]) {
+  ArapSvd o;
+  double Cm[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Cm[i][j] = F[0][i] * F[0][j] + F[1][i] * F[1][j] + F[2][i] * F[2][j];
+  sym3_eig(Cm, o.V);
+  const double dv = o.V[0][0] * (o.V[1][1] * o.V[2][2] - o.V[1][2] * o.V[2][1]) -
+                    o.V[0][1] * (o.V[1][0] * o.V[2][2] - o.V[1][2] * o.V[2][0]) +
+                    o.V[0][2] * (o.V[1][0] * o.V[2][1] - o.V[1][1] * o.V[2][0]);
+  if (dv < 0.0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o.V[k][2] = -o.V[k][2];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    o.s[k] = sqrt(fmax(Cm[k][k], 0.0));
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      o.U[r][k] = (F[r][0] * o.V[0][k] + F[r][1] * o.V[1][k] + F[r][2] * o.V[2][k]) / o.s[k];
+  }
+  return o;
+}
+
 // ------------------------------------------------------------------------------------- K1
 __global__ void __launch_bounds__(kElasticThreads)
 k_elastic(int T, const double* __restrict__ x, const int4* __restrict__ tets,
           const double* __restrict__ Dm_inv, const double* __restrict__ vol,
-          const double* __restrict__ mu_t, const double* __restrict__ lam_t,
+          const double* __restrict__ mu_t, const double* __restrict__ lam_t, const unsigned char* __restrict__ model,
           double* __restrict__ stage, double* __restrict__ grad, double* __restrict__ lbar) {
   extern __shared__ double smem[];
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -99,11 +173,22 @@ k_elastic(int T, const double* __restrict__ x, const int4* __restrict__ tets,
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) A[i][j] = C[i][j] / J;
+  const bool arap = model != nullptr && model[e] == 1;
+  ArapSvd sv;
   double P[3][3];
+  if (arap) {
+    sv = arap_svd(F);
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) P[i][j] = mu * (F[i][j] - A[i][j]) + lam * lnJ * A[i][j];
+      for (int j = 0; j < 3; ++j)
+        P[i][j] = 2.0 * mu * (F[i][j] - (sv.U[i][0] * sv.V[j][0] + sv.U[i][1] * sv.V[j][1] + sv.U[i][2] * sv.V[j][2]));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) P[i][j] = mu * (F[i][j] - A[i][j]) + lam * lnJ * A[i][j];
+  }
   // gradient: dE/dDs = V P Dm^{-T}
   double G[3][3];
 #pragma unroll
@@ -146,16 +231,43 @@ k_elastic(int T, const double* __restrict__ x, const int4* __restrict__ tets,
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int n = 0; n < 3; ++n) B[i][n] = A[i][0] * R3[n][0] + A[i][1] * R3[n][1] + A[i][2] * R3[n][2];
-  const double c2 = mu - lam * lnJ;
   double M[Sym<9>::kSize];
+  if (arap) {
+    // reduced twist vectors w^{ab}_{(m,i)} = sum_j T_ab[i][j] R3[m][j], T_ab = u_a v_b^T - u_b v_a^T
+    double W[3][9], cw[3];
 #pragma unroll
-  for (int al = 0; al < 9; ++al)
+    for (int ab = 0; ab < 3; ++ab) {
+      const int a = ab == 2 ? 1 : 0, b = ab == 0 ? 1 : 2;
+      cw[ab] = 1.0 / (sv.s[a] + sv.s[b]);
 #pragma unroll
-    for (int be = al; be < 9; ++be) {
-      const int m = al / 3, i = al % 3, n = be / 3, k = be % 3;
-      M[Sym<9>::id(al, be)] =
-          Ve * ((i == k ? mu * S[m][n] : 0.0) + c2 * B[i][n] * B[k][m] + lam * B[i][m] * B[k][n]);
+      for (int m = 0; m < 3; ++m)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) t += (sv.U[i][a] * sv.V[j][b] - sv.U[i][b] * sv.V[j][a]) * R3[m][j];
+          W[ab][3 * m + i] = t;
+        }
     }
+#pragma unroll
+    for (int al = 0; al < 9; ++al)
+#pragma unroll
+      for (int be = al; be < 9; ++be) {
+        const int m = al / 3, i = al % 3, n = be / 3, k = be % 3;
+        const double tw = cw[0] * W[0][al] * W[0][be] + cw[1] * W[1][al] * W[1][be] + cw[2] * W[2][al] * W[2][be];
+        M[Sym<9>::id(al, be)] = Ve * 2.0 * mu * ((i == k ? S[m][n] : 0.0) - tw);
+      }
+  } else {
+    const double c2 = mu - lam * lnJ;
+#pragma unroll
+    for (int al = 0; al < 9; ++al)
+#pragma unroll
+      for (int be = al; be < 9; ++be) {
+        const int m = al / 3, i = al % 3, n = be / 3, k = be % 3;
+        M[Sym<9>::id(al, be)] =
+            Ve * ((i == k ? mu * S[m][n] : 0.0) + c2 * B[i][n] * B[k][m] + lam * B[i][m] * B[k][n]);
+      }
+  }
   const double tr = psd_project<9>(M, V, stride);
   lbar[e] = tr / 12.0;
   expand_write<4>(M, stage + 90 * (size_t)e);
@@ -165,7 +277,7 @@ k_elastic(int T, const double* __restrict__ x, const int4* __restrict__ tets,
 __global__ void k_elastic_energy(int T, const double* __restrict__ x, const int4* __restrict__ tets,
                                  const double* __restrict__ Dm_inv, const double* __restrict__ vol,
                                  const double* __restrict__ mu_t, const double* __restrict__ lam_t,
-                                 double* __restrict__ out) {
+                                 const unsigned char* __restrict__ model, double* __restrict__ out) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= T) return;
   const int4 tt = tets[e];
@@ -189,6 +301,11 @@ __global__ void k_elastic_energy(int T, const double* __restrict__ x, const int4
                    F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
   if (!(J > 0.0)) {
     out[e] = INFINITY;
+    return;
+  }
+  if (model != nullptr && model[e] == 1) {  // ARAP: mu (tr F^T F - 2 (s1 + s2 + s3) + 3)
+    const ArapSvd sv = arap_svd(F);
+    out[e] = vol[e] * mu_t[e] * (Ic - 2.0 * (sv.s[0] + sv.s[1] + sv.s[2]) + 3.0);
     return;
   }
   const double lnJ = log(J), mu = mu_t[e], lam = lam_t[e];
@@ -488,8 +605,8 @@ __global__ void k_friction_energy(int n, const double* __restrict__ x, const dou
 size_t elastic_smem(int threads) { return sizeof(double) * 81 * (size_t)threads; }
 
 void launch_elastic(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
-                    const double* vol, const double* mu, const double* lam, double* stage, double* grad,
-                    double* lbar) {
+                    const double* vol, const double* mu, const double* lam, const unsigned char* model,
+                    double* stage, double* grad, double* lbar) {
   if (T <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -500,14 +617,15 @@ void launch_elastic(cudaStream_t st, int T, const double* x, const int4* tets, c
     attr = true;
   }
   k_elastic<<<ceil_div(T, kElasticThreads), kElasticThreads, elastic_smem(kElasticThreads), st>>>(
-      T, x, tets, Dm_inv, vol, mu, lam, stage, grad, lbar);
+      T, x, tets, Dm_inv, vol, mu, lam, model, stage, grad, lbar);
   CK(cudaGetLastError());
 }
 
 void launch_elastic_energy(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
-                           const double* vol, const double* mu, const double* lam, double* out) {
+                           const double* vol, const double* mu, const double* lam, const unsigned char* model,
+                           double* out) {
   if (T <= 0) return;
-  k_elastic_energy<<<ceil_div(T, 256), 256, 0, st>>>(T, x, tets, Dm_inv, vol, mu, lam, out);
+  k_elastic_energy<<<ceil_div(T, 256), 256, 0, st>>>(T, x, tets, Dm_inv, vol, mu, lam, model, out);
   CK(cudaGetLastError());
 }
 

@@ -50,10 +50,11 @@ constexpr int kMaxGroups = 64;
 
 // ---- stencils (k_stencils.cu)
 void launch_elastic(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
-                    const double* vol, const double* mu, const double* lam, double* stage, double* grad,
-                    double* lbar);
+                    const double* vol, const double* mu, const double* lam, const unsigned char* model,
+                    double* stage, double* grad, double* lbar);
 void launch_elastic_energy(cudaStream_t st, int T, const double* x, const int4* tets, const double* Dm_inv,
-                           const double* vol, const double* mu, const double* lam, double* out);
+                           const double* vol, const double* mu, const double* lam, const unsigned char* model,
+                           double* out);
 void launch_contact(cudaStream_t st, int n, const double* x, const int* keys, const double* inA,
                     const double* inAp, const double* mu, const double* s, double sigma, double dhat,
                     double* stage, double* grad, double* lbar, int* nodes, double* dist, double* dphi);

@@ -588,3 +588,22 @@ def twist_targets(scene, t):
         m = scene["twist_end"] == side
         x[m] = x[m] @ rot_axis((0.0, 0.0, 1.0), sign * scene["twist_omega"] * t).T
     return x
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: Neo-Hookean / ARAP coupling (fig:bunny-balls)
+# --------------------------------------------------------------------------
+def make_nh_arap_cubes(seed=1, E_arap=1e6, E_nh=1e4, **kw):
+    """The C1 layout with the bottom cube ARAP (stiff, E = 1 MPa) and the top cube Neo-Hookean (soft,
+    E = 10 kPa) -- the contrast of the paper's NH bunnies in ARAP balls on a scene the
+    oracle steps in seconds.  material_model: 0 = Neo-Hookean, 1 = ARAP (per material)."""
+    sc = make_cubes(seed, **kw)
+    nt = len(sc["tets"]) // 2  # two equal cubes, bottom first
+    nu, rho = sc["materials"][0][1], sc["materials"][0][2]
+    sc["materials"] = np.array([[E_arap, nu, rho], [E_nh, nu, rho]])
+    sc["material_model"] = np.array([1, 0])
+    tm = np.zeros(len(sc["tets"]), np.int32)
+    tm[nt:] = 1
+    sc["tet_material"] = tm
+    sc["name"] = "NH-ARAP-cubes"
+    return sc
