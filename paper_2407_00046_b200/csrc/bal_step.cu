@@ -219,6 +219,11 @@ struct Energy {
 // R-LS1: the line search accepts L(x + a p) <= L(x) + 8u max(S0, S1), i.e. no increase
 // beyond the FP64 evaluation error of L (S = sum of the magnitudes of its terms).
 constexpr double kLsRound = 8.0 * 1.1102230246251565e-16;
+// R-LS1 tolerance factor; BAL_LS_ROUND overrides it (experiments only: 0 = the literal Q35 test)
+inline double ls_round() {
+  static const double v = getenv("BAL_LS_ROUND") ? atof(getenv("BAL_LS_ROUND")) : kLsRound;
+  return v;
+}
 // R-FRIC1: window of the friction-anchor freeze test
 constexpr int kFreezeWindow = 10;
 
@@ -594,7 +599,7 @@ bool frame_iterate(bal_ctx* c, int max_iters) {
                   E1.part[3] - E0.part[3], E1.part[4] - E0.part[4], E1.dmin, E1.count);
         // R-LS1; an infeasible trial (J <= 0, d <= 0, NaN) has L = +inf and is never accepted
         if (E1.count <= P.max_constraints && std::isfinite(E1.L) &&
-            E1.L <= E0.L + kLsRound * std::max(E0.S, E1.S)) {
+            E1.L <= E0.L + ls_round() * std::max(E0.S, E1.S)) {
           ok = true;
           break;
         }
