@@ -42,8 +42,6 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   pin_ptr.upload(H.pin_ptr.data(), H.pin_ptr.size(), st);
   meta.upload(H.meta.data(), std::max<size_t>(H.meta.size(), 16), st);
   part.reserve(3 * (size_t)std::max(H.nslots, 1));
-  wc.reserve(3 * (size_t)N);
-  cdpart.reserve(kVecBlocks);
   plan = TsPlan();
   plan.n = N;
   plan.ntiles = H.ntiles;
@@ -54,8 +52,6 @@ void TsDev::build(int N, const std::vector<int>& lrow, const std::vector<int>& l
   plan.meta = meta.ptr;
   plan.pin_ptr = pin_ptr.ptr;
   plan.part = part.ptr;
-  plan.wc = wc.ptr;
-  plan.cdpart = cdpart.ptr;
   plan.o_meta = H.o_meta;
   plan.o_val = H.o_val;
   plan.o_vt = H.o_vt;

@@ -14,7 +14,7 @@ struct TsDev {
   bal::DevBuf<int> pin_ptr;
   bal::DevBuf<int4> desc;
   bal::DevBuf<unsigned char> meta;
-  bal::DevBuf<double> part, wc, cdpart;
+  bal::DevBuf<double> part;
   bal::TsPlan plan;
   bool ready = false;
   // lower CSR (lrow[N+1], lcol) -> plan on the device; ready = false when the kernel cannot be used

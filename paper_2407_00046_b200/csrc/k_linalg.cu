@@ -709,8 +709,7 @@ template <int NP>
 BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* __restrict__ pin_ptr,
                            const double* __restrict__ part, const double* __restrict__ w, double* __restrict__ u,
                            double* __restrict__ p, double* __restrict__ s, double* __restrict__ x,
-                           double* __restrict__ r, double alpha, double beta, double& g, double& rr, double& xx,
-                           const int* __restrict__ crp, const double* __restrict__ wc) {
+                           double* __restrict__ r, double alpha, double beta, double& g, double& rr, double& xx) {
   constexpr int ND = 3 * NP;
   const size_t d0 = 3 * (size_t)i0;
   double wv[ND], uv[ND], pv[ND], sv[ND], xv[ND], rv[ND];
@@ -747,14 +746,6 @@ BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* _
       }
     }
   }
-  if (crp) {  // contact rows (k_contact_rows, before the tile SpMV): w += wc
-#pragma unroll
-    for (int n = 0; n < NP; ++n)
-      if (crp[i0 + n + 1] > crp[i0 + n]) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) wv[3 * n + c] += wc[3 * (size_t)(i0 + n) + c];
-      }
-  }
 #pragma unroll
   for (int k = 0; k < ND; ++k) {
     pv[k] = uv[k] + beta * pv[k];
@@ -789,8 +780,7 @@ BAL_D void cg_update_nodes(int i0, const double* __restrict__ dinv, const int* _
 __global__ void __launch_bounds__(kVecThreads)
 k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_ptr, const double* __restrict__ part,
             const double* __restrict__ w, double* __restrict__ u, double* __restrict__ p, double* __restrict__ s,
-            double* __restrict__ x, double* __restrict__ r, double* __restrict__ upart, PcgScal* sc,
-            const int* __restrict__ crp, const double* __restrict__ wc) {
+            double* __restrict__ x, double* __restrict__ r, double* __restrict__ upart, PcgScal* sc) {
   if (sc->done) return;
   const double alpha = sc->alpha, beta = sc->beta;
   double g = 0.0, rr = 0.0, xx = 0.0;
@@ -801,10 +791,10 @@ k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_
   const int T = gridDim.x * blockDim.x, t = blockIdx.x * blockDim.x + threadIdx.x;
   if (vec) {
     const int npairs = n / 2;
-    for (int q = t; q < npairs; q += T) cg_update_nodes<2>(2 * q, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx, crp, wc);
-    if ((n & 1) && t == T - 1) cg_update_nodes<1>(n - 1, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx, crp, wc);
+    for (int q = t; q < npairs; q += T) cg_update_nodes<2>(2 * q, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
+    if ((n & 1) && t == T - 1) cg_update_nodes<1>(n - 1, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
   } else {
-    for (int i = t; i < n; i += T) cg_update_nodes<1>(i, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx, crp, wc);
+    for (int i = t; i < n; i += T) cg_update_nodes<1>(i, dinv, pin_ptr, part, w, u, p, s, x, r, alpha, beta, g, rr, xx);
   }
   __shared__ double sh[kVecThreads / 32];
   const double bg = block_sum<kVecThreads>(g, sh);
@@ -821,8 +811,8 @@ k_cg_update(int n, const double* __restrict__ dinv, const int* __restrict__ pin_
 
 void launch_cg_update(cudaStream_t st, int n, const double* dinv, const int* pin_ptr, const double* part,
                       const double* w, double* u, double* p, double* s, double* x, double* r, double* upart,
-                      PcgScal* sc, const int* crp, const double* wc) {
-  k_cg_update<<<kVecBlocks, kVecThreads, 0, st>>>(n, dinv, pin_ptr, part, w, u, p, s, x, r, upart, sc, crp, wc);
+                      PcgScal* sc) {
+  k_cg_update<<<kVecBlocks, kVecThreads, 0, st>>>(n, dinv, pin_ptr, part, w, u, p, s, x, r, upart, sc);
   CK(cudaGetLastError());
 }
 

@@ -25,7 +25,6 @@
 // together with the (r, u) and (r, r) block partials of the preceding PCG update kernel -- the
 // one grid-wide reduction of a Chronopoulos-Gear PCG iteration.
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -284,7 +283,6 @@ struct TsArgs {
   const double* upart;
   double* hist;
   int cpref;  // producer prefetches each tile's contact range (values, columns) into L2
-  const double* cdpart;  // [kVecBlocks] (v, C v) block partials of k_contact_rows, or null
 };
 
 // sum of the 3-vectors p[3b .. 3e) into (s0, s1, s2), four independent partial sums (short
@@ -580,8 +578,6 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       const bool wx = a.sc->crit == 2;  // criterion (ii) needs ||x_k||: (x,x) partials after the pairs
       double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
       for (int i = tid; i < G; i += kTsThreads) t0 += a.dpart[i];
-      if (a.cdpart)
-        for (int i = tid; i < kVecBlocks; i += kTsThreads) t0 += a.cdpart[i];
       for (int i = tid; i < kVecBlocks; i += kTsThreads) {
         t1 += a.upart[2 * i];
         t2 += a.upart[2 * i + 1];
@@ -600,64 +596,17 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
 }
 
 __global__ void __launch_bounds__(kVecThreads)
-k_ts_combine(int n, const int* __restrict__ pin_ptr, const double* __restrict__ part, double* __restrict__ y,
-             const int* __restrict__ crp, const double* __restrict__ wc) {
+k_ts_combine(int n, const int* __restrict__ pin_ptr, const double* __restrict__ part, double* __restrict__ y) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int e0 = pin_ptr[i], e1 = pin_ptr[i + 1];
-    const bool hc = crp != nullptr && crp[i + 1] > crp[i];
-    if (e0 == e1 && !hc) continue;
+    if (e0 == e1) continue;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       double acc = y[3 * (size_t)i + c];
       for (int e = e0; e < e1; ++e) acc += part[3 * (size_t)e + c];
-      if (hc) acc += wc[3 * (size_t)i + c];
       y[3 * (size_t)i + c] = acc;
     }
   }
-}
-
-// Contact rows of y = C v, one thread per row, the row's blocks in column order (row-sorted contact
-// BSR, both triangles): wc[i] = sum_s C_is v_col(s) for rows with contact blocks; the (v, wc) block
-// partials feed the single-reduction PCG (exactly kVecBlocks blocks, summed by the tile kernel's last
-// CTA).  Streams each contact block once with the contiguous per-row ranges, off the tile kernel's
-// critical path (its consumers otherwise wait on these global loads, profiles/spmv_variants_r02.md).
-__global__ void __launch_bounds__(kVecThreads)
-k_contact_rows(int n, const int* __restrict__ crp, const int* __restrict__ col, const double* __restrict__ val,
-               const double* __restrict__ v, double* __restrict__ wc, double* __restrict__ cdpart) {
-  double dot = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int e0 = crp[i], e1 = crp[i + 1];
-    if (e0 == e1) continue;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int s = e0; s < e1; ++s) {
-      const double* A = val + 9 * (size_t)s;
-      const double* vc = v + 3 * (size_t)__ldg(col + s);
-      const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);
-      a0 = fma(__ldg(A + 2), c2, fma(__ldg(A + 1), c1, fma(__ldg(A), c0, a0)));
-      a1 = fma(__ldg(A + 5), c2, fma(__ldg(A + 4), c1, fma(__ldg(A + 3), c0, a1)));
-      a2 = fma(__ldg(A + 8), c2, fma(__ldg(A + 7), c1, fma(__ldg(A + 6), c0, a2)));
-    }
-    double* w = wc + 3 * (size_t)i;
-    w[0] = a0;
-    w[1] = a1;
-    w[2] = a2;
-    if (cdpart) dot += v[3 * (size_t)i] * a0 + v[3 * (size_t)i + 1] * a1 + v[3 * (size_t)i + 2] * a2;
-  }
-  if (cdpart) {
-    __shared__ double sh[kVecThreads / 32];
-    const double bs = block_sum<kVecThreads>(dot, sh);
-    if (threadIdx.x == 0) cdpart[blockIdx.x] = bs;
-  }
-}
-
-bool ts_contact_separate() {  // BAL_TS_CONTACT_INLINE=1: contacts inside the tile kernel (round-2 A/B)
-  static const bool sep = getenv("BAL_TS_CONTACT_INLINE") == nullptr;
-  return sep;
-}
-
-void launch_contact_rows(cudaStream_t st, const Bsr& C, const double* v, double* wc, double* cdpart) {
-  k_contact_rows<<<kVecBlocks, kVecThreads, 0, st>>>(C.n, C.row_ptr, C.col, C.val, v, wc, cdpart);
-  CK(cudaGetLastError());
 }
 
 namespace {
@@ -700,12 +649,8 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
                     bool combine) {
   const int g = ts_grid<false>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  const bool sep = ts_contact_separate() && C.nnzb > 0 && combine;
-  if (sep) launch_contact_rows(st, C, v, S.ts->wc, nullptr);
-  Bsr Ct = C;
-  if (sep) Ct = Bsr{};
-  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, Ct, v, y, part,
-           nullptr, nullptr, nullptr, nullptr, nullptr, ts_cpref(), nullptr};
+  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, v, y, part,
+           nullptr, nullptr, nullptr, nullptr, nullptr, ts_cpref()};
 #ifdef BAL_TS_TIMING
   unsigned long long z[16] = {0};
   CK(cudaMemcpyToSymbolAsync(g_ts_timing, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
@@ -722,8 +667,7 @@ void launch_spmv_ts(cudaStream_t st, const Bsr& S, const Bsr& C, const double* v
           z[13] / 1e3 / g, z[14] / 1e3 / g, z[9] / 1e3 / g, z[10] / 1e3 / g, z[15] / 1e3 / g);
 #endif
   if (combine) {
-    k_ts_combine<<<kVecBlocks, kVecThreads, 0, st>>>(S.n, S.ts->pin_ptr, part, y, sep ? C.row_ptr : nullptr,
-                                                     S.ts->wc);
+    k_ts_combine<<<kVecBlocks, kVecThreads, 0, st>>>(S.n, S.ts->pin_ptr, part, y);
     CK(cudaGetLastError());
   }
 }
@@ -732,12 +676,8 @@ void launch_spmv_ts_dot(cudaStream_t st, const Bsr& S, const Bsr& C, const doubl
                         double* dpart, unsigned* counter, PcgScal* sc, const double* upart, double* hist) {
   const int g = ts_grid<true>(*S.ts);
   if (g <= 0) throw CudaError("k_spmv_ts: no resident CTA (shared memory)");
-  const bool sep = ts_contact_separate() && C.nnzb > 0;
-  if (sep) launch_contact_rows(st, C, u, S.ts->wc, S.ts->cdpart);
-  Bsr Ct = C;
-  if (sep) Ct = Bsr{};
-  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, Ct, u, w, part, dpart,
-           counter, sc, upart, hist, ts_cpref(), sep ? S.ts->cdpart : nullptr};
+  TsArgs a{*S.ts, S.ts->val_bytes == 36 ? (const void*)S.val32 : (const void*)S.val, C, u, w, part, dpart,
+           counter, sc, upart, hist, ts_cpref()};
   ts_launch<true>(g, st, a);
   CK(cudaGetLastError());
 }

@@ -101,11 +101,6 @@ struct TsPlan {
   const unsigned char* meta = nullptr;
   const int* pin_ptr = nullptr;        // [n+1] partial slots targeting row j: [pin_ptr[j], pin_ptr[j+1])
   double* part = nullptr;              // [3 nslots] work buffer of the partials (owned by the ctx)
-  // contact rows computed by k_contact_rows before the tile kernel (default; BAL_TS_CONTACT_INLINE=1
-  // keeps them inside the tile kernel): wc[3 i] = sum_s C_is v_col(s) for rows with contact blocks,
-  // cdpart[kVecBlocks] its (v, wc) block partials for the single-reduction PCG
-  double* wc = nullptr;
-  double* cdpart = nullptr;
   int cap_nb = 0, cap_rows = 0, cap_cs = 0, cap_tp = 0;
   int val_bytes = 72;  // 72: FP64 stored blocks; 36: FP32 (BAL_FP32_MATRIX, FP64 arithmetic)
   size_t o_crp = 0;  // contact row pointers of the tile (cp.async with the out-of-tile v)
@@ -145,10 +140,7 @@ void launch_cg_init(cudaStream_t st, int n, const double* b, const double* Ax0, 
                     PcgScal* sc, double* hist, const double* x);
 void launch_cg_update(cudaStream_t st, int n, const double* dinv, const int* pin_ptr, const double* part,
                       const double* w, double* u, double* p, double* s, double* x, double* r, double* upart,
-                      PcgScal* sc, const int* crp = nullptr, const double* wc = nullptr);
-// contact rows of y = C v (k_spmv_ts.cu): wc for rows with contact blocks, optional (v, wc) block partials
-void launch_contact_rows(cudaStream_t st, const Bsr& C, const double* v, double* wc, double* cdpart);
-bool ts_contact_separate();
+                      PcgScal* sc);
 
 // static-part SpMV layout: 0 = symmetric (lower + mirror index), 1 = full BSR streamed by the tiled
 // kernel, 2 = full BSR staged through shared memory with cp.async.  BAL_SPMV=sym|full|staged.

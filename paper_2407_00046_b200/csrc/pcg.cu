@@ -146,9 +146,8 @@ static void capture_batch(bal_ctx* c, const Bsr& S, const Bsr& C, int set, cudaG
     if (cg) {
       // Chronopoulos-Gear: update k (x, r, u, p, s) then SpMV k+1 (w = A u, the iteration's one
       // grid-wide reduction, App. B stop test, alpha / beta)
-      const bool csep = ts_contact_separate() && C.nnzb > 0;  // contact rows in w via wc (k_contact_rows)
       launch_cg_update(st, N, c->dinv.ptr, S.ts->pin_ptr, S.ts->part, c->pq.ptr, c->pz.ptr, c->pp.ptr, c->ps.ptr,
-                       c->px.ptr, c->pr.ptr, c->upart.ptr, c->scal.ptr, csep ? C.row_ptr : nullptr, S.ts->wc);
+                       c->px.ptr, c->pr.ptr, c->upart.ptr, c->scal.ptr);
       if (as_on(c)) launch_as_apply(st, N, c->as_inv.ptr, c->pr.ptr, c->pz.ptr, c->upart.ptr, c->scal.ptr);
       if (it < kTimedPerBatch) CK(cudaEventRecordWithFlags(ev[2 * it], st, cudaEventRecordExternal));
       launch_spmv_ts_dot(st, S, C, c->pz.ptr, c->pq.ptr, S.ts->part, c->dpart.ptr, c->counter.ptr, c->scal.ptr,
@@ -187,9 +186,7 @@ static void run_batches(bal_ctx* c, const Bsr& S, const Bsr& C, bal_pcg_stats* s
   int k_prev = c->h_scal->k;
   CK(cudaGraphLaunch(ge[0], st));
   CK(cudaGraphLaunch(ge[1], st));
-  const int per_iter = (ts_usable(S) || pcg_fused_grid(c->N) > 0)
-                           ? 2 + (as_on(c) ? 1 : 0) + ((ts_usable(S) && ts_contact_separate() && C.nnzb > 0) ? 1 : 0)
-                           : 3;
+  const int per_iter = (ts_usable(S) || pcg_fused_grid(c->N) > 0) ? 2 + (as_on(c) ? 1 : 0) : 3;
   c->launches += 2 * per_iter * kBatch;
   int cur = 0;
   while (true) {
