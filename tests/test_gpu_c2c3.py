@@ -39,7 +39,7 @@ def _np(t):
 
 def _sub_mesh(m, sel):
     return type(m)(**{**m.__dict__, "tets": m.tets[sel], "Dm_inv": m.Dm_inv[sel], "vol": m.vol[sel],
-                      "mu": m.mu[sel], "lam": m.lam[sel]})
+                      "mu": m.mu[sel], "lam": m.lam[sel], "arap": m.arap[sel]})
 
 
 @pytest.fixture(scope="module", params=["c2", "c3"])

@@ -49,7 +49,7 @@ def c4():
 
 def _sub_mesh(m, sel):
     return type(m)(**{**m.__dict__, "tets": m.tets[sel], "Dm_inv": m.Dm_inv[sel], "vol": m.vol[sel],
-                      "mu": m.mu[sel], "lam": m.lam[sel]})
+                      "mu": m.mu[sel], "lam": m.lam[sel], "arap": m.arap[sel]})
 
 
 def test_c4_sampled_elastic_stencils(c4):
