@@ -164,7 +164,7 @@ def oracle_sample(sc, newton_per_frame, pcg_per_newton, budget_tets=20000, seed=
     T = len(m.tets)
     sel = rng.choice(T, size=min(budget_tets, T), replace=False)
     sub = type(m)(**{**m.__dict__, "tets": m.tets[sel], "Dm_inv": m.Dm_inv[sel], "vol": m.vol[sel],
-                     "mu": m.mu[sel], "lam": m.lam[sel]})
+                     "mu": m.mu[sel], "lam": m.lam[sel], "arap": m.arap[sel]})
     x = np.asarray(sc["x0"], np.float64)
     t0 = time.perf_counter()
     _v, _g, H = nh_stencils(x, sub)

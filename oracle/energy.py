@@ -96,6 +96,8 @@ def nh_stencils(x, mesh, chunk=20000):
     grad = np.empty((T, 12))
     hess = np.empty((T, 12, 12))
     arap = mesh.arap if mesh.arap is not None else np.zeros(T, bool)
+    if len(arap) != T:
+        raise ValueError("mesh.arap must have one entry per tet (subset it with the tets)")
     for model in (False, True):
         idx = np.nonzero(arap == model)[0]
         for s in range(0, len(idx), chunk):
