@@ -471,20 +471,6 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       double* cs = reinterpret_cast<double*>(sm + a.P.o_scratch) +
                    (size_t)(it % kTsScratchBufs) * 3 * (a.P.cap_cs + a.P.cap_tp + kTsContactCap);
       double* tp = cs + 3 * (size_t)a.P.cap_cs;
-#if BAL_TS_CEARLY
-      // issue the first contact block's column and v loads before phase 1 (consumed after it), so the
-      // dependent col -> v latency hides behind the static products
-      const int* cr0 = reinterpret_cast<const int*>(S + a.P.o_crp);
-      const int c0e = crp ? cr0[0] : 0;
-      const int ncce = crp ? min(cr0[R] - c0e, kTsContactCap) : 0;
-      double ev0 = 0.0, ev1 = 0.0, ev2 = 0.0;
-      if (ct < ncce) {
-        const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + (size_t)(c0e + ct));
-        ev0 = __ldg(vc);
-        ev1 = __ldg(vc + 1);
-        ev2 = __ldg(vc + 2);
-      }
-#endif
       // ---- phase 1, one thread per stored block A_ij (i = r0 + il, j <= i): cs[q] = A v_j; an
       // off-diagonal block also writes A^T v_i to its slot tp[tslot[q]] (grouped by target row)
       for (int q = ct; q < nb; q += kTsConsumers) {
@@ -520,21 +506,11 @@ __global__ void __launch_bounds__(kTsThreads, kTsMinBlocks) k_spmv_ts(const TsAr
       for (int e = ct; e < ncc; e += kTsConsumers) {
         const size_t s2 = (size_t)(c0r + e);
         const double* A = a.C.val + 9 * s2;
+        const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
         double m[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) m[k] = __ldg(A + k);
-#if BAL_TS_CEARLY
-        double c0 = ev0, c1 = ev1, c2 = ev2;
-        if (e != ct) {
-          const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
-          c0 = __ldg(vc);
-          c1 = __ldg(vc + 1);
-          c2 = __ldg(vc + 2);
-        }
-#else
-        const double* vc = a.v + 3 * (size_t)__ldg(a.C.col + s2);
         const double c0 = __ldg(vc), c1 = __ldg(vc + 1), c2 = __ldg(vc + 2);
-#endif
         cc[3 * e] = fma(m[2], c2, fma(m[1], c1, m[0] * c0));
         cc[3 * e + 1] = fma(m[5], c2, fma(m[4], c1, m[3] * c0));
         cc[3 * e + 2] = fma(m[8], c2, fma(m[7], c1, m[6] * c0));

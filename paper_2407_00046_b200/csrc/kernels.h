@@ -36,9 +36,6 @@ constexpr int kTsStages = BAL_TS_STAGES;
 #define BAL_TS_SCRATCH_BUFS 1
 #endif
 constexpr int kTsScratchBufs = BAL_TS_SCRATCH_BUFS;
-#ifndef BAL_TS_CEARLY
-#define BAL_TS_CEARLY 0  // contact column / v loads issued before phase 1 (experiment)
-#endif
 #ifndef BAL_TS_CONTACT_CAP
 #define BAL_TS_CONTACT_CAP 384
 #endif
