@@ -137,3 +137,14 @@ def test_degenerate_step_parity(name):
     pt, ee = cm.candidates(o.mesh, xg, xg, o.dhat)
     _k, d = cm.constraint_set(xg, pt, ee, o.dhat)
     assert np.all(d > 0)
+
+
+def test_detect_rejects_a_short_output_buffer():
+    """bal_detect (include/bal.h): |A| > max_n is BAL_E_INVALID_ARG, and *n_out still reports |A|."""
+    sc = scene("vertex_over_vertex")
+    ctx = bal.bal_init(sc)
+    keys, _d = bal.bal_detect(ctx, _t(sc["x0"]))
+    assert len(keys) > 1
+    with pytest.raises(bal.BalError) as ei:
+        bal.bal_detect(ctx, _t(sc["x0"]), max_n=1)
+    assert ei.value.status == -1
